@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark of the PipeSP attention layer (BASELINE.json metric) -- one JSON line on rank 0.
+
+    python bench.py [--gpus N --steps K --warmup W] [--workload osp480p93f] [--stages N_st]
+    torchrun --nproc-per-node N bench.py --gpus N ...           (one process per GPU, NCCL)
+    python bench.py --impl reference ...                         (the fp64 CPU oracle arm)
+
+A step = one SP attention layer (all SURVEY §8(a) rows: pack, per-stage input all-to-all,
+tcgen05 attention, per-stage output all-to-all, Psi_g unpack) over one batch of synthetic
+Q/K/V shaped like the named workload, inputs resident in HBM.  Strong scaling: the global
+problem (B, S, H, D) is fixed and split over P = N ranks.  `value` = total attention FLOPs
+(4*B*S^2*H*D) / max-over-ranks step time, in TFLOP/s.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms per SP attention layer and TFLOP/s at 1/2/4/8 B200; exposed all-to-all %"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="osp480p93f")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--stages", type=int, default=0, help="N_st (0 = paper's per-head loop, h stages)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def workload_cfg(args):
+    import synthgen
+    w = synthgen.WORKLOADS[args.workload]
+    B = args.batch or w.B
+    return w.name, B, w.S, w.H, w.D
+
+
+def attn_flops(B, S, H, D):
+    return 4.0 * B * S * S * H * D
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU oracle timing
+def time_oracle(S, D, rows_target_s: float, seed=0):
+    """The fp64 C oracle (as it stands) on R query rows of one head with the full K/V of that head."""
+    import numpy as np
+    import torch
+
+    import oracle
+    import synthgen
+    shape = (1, S, 1, D)
+    K = synthgen.gen_head_rows(seed, synthgen.TENSOR_K, shape, 0, 0).double().numpy()
+    V = synthgen.gen_head_rows(seed, synthgen.TENSOR_V, shape, 0, 0).double().numpy()
+    nthreads = os.cpu_count() or 1
+    probe = max(nthreads, 16)
+    Q = synthgen.gen_head_rows(seed, synthgen.TENSOR_Q, shape, 0, 0, tokens=torch.arange(probe)).double().numpy()
+    t0 = time.perf_counter()
+    oracle.attention_rows(Q, K, V, nthreads)
+    dt = time.perf_counter() - t0
+    R = int(max(probe, min(65536, probe * rows_target_s / max(dt, 1e-6))))
+    R = (R // nthreads) * nthreads or nthreads
+    rows = torch.arange(R) % S
+    Q = synthgen.gen_head_rows(seed, synthgen.TENSOR_Q, shape, 0, 0, tokens=rows).double().numpy()
+    t0 = time.perf_counter()
+    oracle.attention_rows(Q, K, V, nthreads)
+    dt = time.perf_counter() - t0
+    flops = 4.0 * S * D * R
+    return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": nthreads, "kind": "oracle",
+            "sample": f"{R} query rows x 1 head, full S={S} keys, D={D}, fp64 C oracle, {dt:.1f} s "
+                      f"(full layer extrapolates x{1.0:.0f} per row)", "seconds": dt, "rows": R}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    name, B, S, H, D = workload_cfg(args)
+    if rank != 0:
+        return
+    P = args.gpus
+    res_steps = []
+    per_step_target = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for i in range(args.warmup + args.steps):
+        r = time_oracle(S, D, per_step_target, seed=i)
+        if i >= args.warmup:
+            res_steps.append(r)
+    flops = sum(4.0 * S * D * r["rows"] for r in res_steps)
+    secs = sum(r["seconds"] for r in res_steps)
+    value = flops / secs / 1e12
+    full_layer_s = attn_flops(B, S, H, D) / (value * 1e12)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": P,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": full_layer_s * 1e3 / 1,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded splitmix64 Irwin-Hall bf16 inputs)",
+        "config": {"workload": name, "B": B, "S": S, "H": H, "D": D, "P": P,
+                   "note": "ms_per_step extrapolated from the sampled rows to the full layer"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": res_steps[0]["cores"], "kind": "oracle",
+                         "sample": f"{args.steps} steps x ~{res_steps[0]['rows']} query rows of one head, full K/V"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import synthgen
+    from paper_2511_12056_b200 import spa
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    name, B, S, H, D = workload_cfg(args)
+    P = world
+    if S % P or H % P:
+        raise SystemExit(f"workload {name} does not split over {P} ranks")
+    h, S_l = H // P, S // P
+    stages = args.stages or (h if P > 1 else 1)
+
+    # rank's shard of the global synthetic problem, generated on the device
+    qkv = [synthgen.gen_qkv_shard(0, t, (B, S, H, D), rank * S_l, (rank + 1) * S_l, device=dev) for t in range(3)]
+    out = torch.empty_like(qkv[0])
+    if P == 1:
+        comm = spa.Comm.loopback(1, local)
+    else:
+        obj = [spa.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = spa.Comm.nccl(obj[0], P, rank, local)
+    plan = spa.Plan(comm, B, S, H, D, stages=stages)
+    ws = plan.workspace(dev)
+    stream = torch.cuda.current_stream()
+
+    def step(q, k, v, o):
+        if P == 1:
+            spa.spa_pipesp_attention_local(plan, [q], [k], [v], [o], ws, stream)
+        else:
+            spa.spa_pipesp_attention(plan, q, k, v, o, ws, stream)
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(*qkv, out)
+    barrier()
+
+    plan.set_option(spa.SPA_OPT_PROFILE, 1)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    attn_ms, attn_launches, copy_launches, a2a_in, a2a_out = [], 0, 0, [], []
+    with ClockSampler(local) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()                       # L2 flush between timed steps (untimed)
+            ev[i][0].record(stream)
+            step(*qkv, out)
+            ev[i][1].record(stream)
+            torch.cuda.synchronize()
+            prof = plan.last_profile()
+            attn_ms.append(sum(prof.attn_ms[k] for k in range(prof.n_stages)))
+            a2a_in.append(sum(prof.a2a_in_ms[k] for k in range(prof.n_stages)))
+            a2a_out.append(sum(prof.a2a_out_ms[k] for k in range(prof.n_stages)))
+            attn_launches += prof.attn_launches
+            copy_launches += prof.copy_launches
+        barrier()
+    plan.set_option(spa.SPA_OPT_PROFILE, 0)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_rank = sum(step_ms) / len(step_ms)
+    t = torch.tensor([t_rank], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    flops = attn_flops(B, S, H, D)
+    value = flops / (t_max * 1e-3) / 1e12
+
+    # exposed all-to-all: same plan and schedule with the transport skipped
+    exposed = None
+    if P > 1:
+        plan.set_option(spa.SPA_OPT_SKIP_COMM, 1)
+        for _ in range(2):
+            step(*qkv, out)
+        barrier()
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for i in range(args.steps):
+            flush.zero_()
+            ev2[i][0].record(stream)
+            step(*qkv, out)
+            ev2[i][1].record(stream)
+        barrier()
+        plan.set_option(spa.SPA_OPT_SKIP_COMM, 0)
+        t2 = torch.tensor([sum(a.elapsed_time(b) for a, b in ev2) / args.steps], device=dev)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        exposed = max(0.0, (t_max - float(t2.item())) / t_max * 100.0)
+
+    # end-to-end through the public API with host buffers: H2D inputs, the call, D2H output
+    e2e = None
+    if not args.no_e2e:
+        hq = [x.cpu().pin_memory() for x in qkv]
+        hout = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        dq = [torch.empty_like(x) for x in qkv]
+        dout = torch.empty_like(out)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.steps):
+            for d_, h_ in zip(dq, hq):
+                d_.copy_(h_, non_blocking=True)
+            step(*dq, dout)
+            hout.copy_(dout, non_blocking=True)
+        e1.record(stream)
+        barrier()
+        te = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": flops / (float(te.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "ms_per_step": float(te.item()),
+               "h2d_bytes_per_step": sum(x.numel() * x.element_size() for x in hq),
+               "d2h_bytes_per_step": hout.numel() * hout.element_size()}
+
+    # roofline of the dominant kernel (attention): algorithmic FLOPs per launch / measured duration
+    peaks, peak_src = load_peaks()
+    rank_attn_flops = attn_flops(B, S, H, D) / P
+    attn_ms_avg = sum(attn_ms) / len(attn_ms)
+    achieved = rank_attn_flops / (attn_ms_avg * 1e-3) / 1e12
+    peak = peaks["bf16_tflops"]
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(f"{name}/P{P}/D{D}")
+    except Exception:
+        pass
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": f"{peak_src} bf16_tflops (burst cuBLAS 8192^3)",
+                "frac_of_sustained": achieved / peaks.get("bf16_tflops_sustained", peak),
+                "frac_of_datasheet_2250": achieved / 2250.0, "kernel": "attn_fwd_kernel (tcgen05)",
+                "attn_ms_per_step": attn_ms_avg}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = time_oracle(S, D, args.cpu_seconds)
+        cpu.pop("seconds", None)
+        cpu.pop("rows", None)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded splitmix64 Irwin-Hall, D0, seed 0)",
+            "config": {"workload": name, "B": B, "S": S, "H": H, "D": D, "P": P, "stages": stages,
+                       "stage_split": list(plan.stage_split), "parallelism": f"ulysses-sp{P}" if P > 1 else "single",
+                       "l2": "flushed between timed steps (256 MiB memset, untimed); inputs > L2"},
+            "exposed_a2a_pct": exposed,
+            "a2a_ms_per_step": {"in": sum(a2a_in) / len(a2a_in), "out": sum(a2a_out) / len(a2a_out)} if P > 1 else None,
+            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": attn_launches + copy_launches,
+            "roofline": roofline, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,211 @@
+/*
+ * spa.h -- C ABI of the B200-native PipeSP sequence-parallel attention library
+ * (libspa.so, built from paper_2511_12056_b200/csrc/).
+ *
+ * What the library computes (PAPER.md = /root/reference/PAPER.md):
+ *   Each of P ranks holds a sequence shard Q_r, K_r, V_r of shape [B, S/P, H, D]
+ *   (bf16, contiguous).  Every rank receives its sequence shard of
+ *       O = softmax(Q K^T / sqrt(D)) V        per batch b and head k,
+ *   i.e. O[:, r*S/P:(r+1)*S/P, :, :] in the same [B, S/P, H, D] layout.
+ *   - Ulysses SP (Fig. 3(a)): seq->head all-to-all of Q, K, V,
+ *     attention over the full sequence on H/P local heads, head->seq all-to-all.
+ *   - PipeSP (Alg. 1): the same result, with the attention split
+ *     into N_st pipeline stages; stage k's output all-to-all (and stage k+1's input
+ *     all-to-all) overlap stage k+1's (k's) attention.  The paper's per-head order
+ *     fix view->permute->view (proof PAPER.md:516-578) is fused
+ *     into the final gather, so the interleaved layout is never materialised.
+ *   - Aco (Fig. 4): attention of the heads is spread over
+ *     N_src "denoising" ranks plus spare "decoding" ranks; only source ranks hold
+ *     input and output shards.
+ *   The softmax scale 1/sqrt(D) is the north star's (the paper never states it).
+ *
+ * Numerics: bf16 inputs, fp32 QK^T accumulation and fp32 online softmax, P rounded
+ * to bf16 for the PV product, fp32 O accumulation, bf16 (RNE) output.  Tolerance
+ * vs the fp64 definition: max-abs 2e-2 and rel-L2 5e-3 (BASELINE.json north_star).
+ * The resharding steps are pure permutations: bit-exact.
+ *
+ * Conventions
+ *   - All functions return spa_status; SPA_OK == 0.  Argument / shape errors are
+ *     detected synchronously and NOTHING is enqueued.  spa_last_error() returns a
+ *     thread-local message for the last failing call on this thread.
+ *   - Device pointers: 16-byte aligned, caller-owned (e.g. torch tensors).  The
+ *     library owns comms, plans, its comm stream and events.
+ *   - Stream-ordered: work is enqueued after prior work on `stream` and the output
+ *     is valid when `stream` reaches the end of the call; inputs must not be
+ *     modified before that.  Calls return as soon as everything is enqueued.
+ *   - Collective: with an NCCL comm every rank must call with identical plans in the
+ *     same order (like NCCL itself).
+ *   - Determinism: identical inputs give bit-identical outputs, for any rank count
+ *     and any stage count (each output row depends only on its own query row and
+ *     the full K/V of its head, evaluated in a fixed key-tile order).
+ *   - Not thread-safe per plan: one call at a time per plan.
+ */
+#ifndef SPA_H_
+#define SPA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SPA_OK = 0,
+    SPA_ERR_INVALID = 1,     /* null pointer, bad enum, misaligned pointer, wrong comm kind */
+    SPA_ERR_SHAPE = 2,       /* S % n_src != 0, H % n_owners != 0, stages < 1, query chunks > S/n_src */
+    SPA_ERR_UNSUPPORTED = 3, /* D not in {64, 96, 128}, op not available on this comm kind */
+    SPA_ERR_CUDA = 4,        /* CUDA runtime/driver error (incl. a previous async kernel fault) */
+    SPA_ERR_COMM = 5,        /* NCCL error or async communicator failure */
+    SPA_ERR_BUSY = 6         /* Aco co-processor group busy: caller falls back to PipeSP */
+} spa_status;
+
+typedef struct spa_comm spa_comm; /* rank group ("RankGroup") */
+typedef struct spa_plan spa_plan;
+
+/* ------------------------------------------------------------------ rank groups */
+/* NCCL unique id (128 bytes) created on rank 0; the caller broadcasts it (torch.distributed). */
+spa_status spa_get_unique_id(uint8_t id[128]);
+/* One process per GPU: NCCL communicator of `nranks` ranks over NVLink/NVSwitch; `device` = CUDA ordinal. */
+spa_status spa_comm_init(spa_comm **comm, const uint8_t id[128], int nranks, int rank, int device);
+/* `nvirtual` virtual ranks on ONE GPU (tests / single-GPU measurement): the all-to-all
+ * becomes device-to-device copies on the comm stream, everything else is identical. */
+spa_status spa_comm_init_loopback(spa_comm **comm, int nvirtual, int device);
+/* Host-only rank group: plans can be created, validated and described (spa_plan_describe_*),
+ * but not executed.  Used to test the multi-rank host logic without a GPU. */
+spa_status spa_comm_init_host(spa_comm **comm, int nranks, int rank);
+/* Sub-group (e.g. the denoising group for Aco's busy fallback): ranks with the same
+ * color form a group ordered by key; color < 0 -> *sub = NULL.  NCCL: ncclCommSplit. */
+spa_status spa_comm_split(spa_comm *comm, int color, int key, spa_comm **sub);
+/* Polls the communicator for asynchronous errors (NCCL async error / CUDA sticky error). */
+spa_status spa_comm_check(spa_comm *comm);
+spa_status spa_comm_destroy(spa_comm *comm);
+/* rank count / own rank (-1 for loopback, which holds all ranks). */
+spa_status spa_comm_info(const spa_comm *comm, int *nranks, int *rank, int *kind /* 0 nccl,1 loopback,2 host */);
+
+/* ------------------------------------------------------------------ plans */
+typedef struct {
+    int B, S, H, D; /* global problem: batch, sequence length, heads, head dim (bf16) */
+    int stages;     /* N_st pipeline stages (R7): G_h = gcd(N_st, h) head groups of
+                       g = h/G_h heads, C = N_st/G_h query chunks; 1 = Ulysses (one stage) */
+    int n_src;      /* ranks holding sequence shards: 0 = all ranks (Ulysses/PipeSP);
+                       0 < n_src < nranks = Aco (ranks >= n_src are co-processors) */
+} spa_shape;
+
+/* Validates everything synchronously.  Requirements: D in {64,96,128}; S % n_src == 0;
+ * H % nranks == 0 (heads are split over ALL ranks, which own contiguous head blocks);
+ * 1 <= stages and C <= S/n_src. */
+spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *shape);
+/* Device workspace bytes the caller must pass as `ws` (per rank; for loopback plans:
+ * for all virtual ranks together).  Zero when nranks == 1. */
+spa_status spa_plan_workspace_bytes(const spa_plan *plan, size_t *bytes);
+/* G_h, C, g of the plan's stage split. */
+spa_status spa_plan_stage_split(const spa_plan *plan, int *G_h, int *C, int *g);
+spa_status spa_plan_destroy(spa_plan *plan);
+
+/* Measurement knobs (bench only; never change results except SKIP_COMM).
+ *   SPA_OPT_PROFILE   1 -> record CUDA events around every step of the next calls
+ *   SPA_OPT_SKIP_COMM 1 -> the all-to-alls are not issued (exposed-comm measurement;
+ *                          the output is then NOT the attention result)
+ *   SPA_OPT_COPROC_BUSY 1 -> the decoding group is busy (Fig. 4 prompt-2 stage): spa_aco_*
+ *                          return SPA_ERR_BUSY without enqueueing; the caller runs PipeSP on
+ *                          the denoising sub-group instead */
+enum { SPA_OPT_PROFILE = 1, SPA_OPT_SKIP_COMM = 2, SPA_OPT_COPROC_BUSY = 3 };
+spa_status spa_plan_set_option(spa_plan *plan, int option, int value);
+
+/* Per-step device times (ms) of the last profiled call, once its stream has completed.
+ * attn_ms[k], a2a_in_ms[k], a2a_out_ms[k] for k < n_stages (arrays of >= 64 entries). */
+typedef struct {
+    int n_stages;
+    float total_ms;   /* whole call, first to last event on the caller's stream */
+    float pack_ms, unpack_ms;
+    float attn_ms[64], a2a_in_ms[64], a2a_out_ms[64];
+    int attn_launches, copy_launches; /* library kernels launched by the call */
+} spa_profile;
+spa_status spa_plan_last_profile(spa_plan *plan, spa_profile *out);
+
+/* ------------------------------------------------------------------ SP attention (per-rank collective calls)
+ * q, k, v, out: device bf16 [B, S/n_src, H, D] contiguous (this rank's shard); ws: device
+ * workspace of spa_plan_workspace_bytes(); stream: cudaStream_t of the caller.
+ * NCCL plans only (loopback plans use the *_local variants). */
+spa_status spa_ulysses_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out,
+                                 void *ws, void *stream);
+spa_status spa_pipesp_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out,
+                                void *ws, void *stream);
+/* Aco: plan with 0 < n_src < nranks.  Ranks < n_src pass their shards;
+ * co-processor ranks (>= n_src) pass NULL for q, k, v, out. */
+spa_status spa_aco_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out,
+                             void *ws, void *stream);
+
+/* Loopback plans: arrays with one pointer per source rank (n_src entries, or nranks when
+ * n_src == 0); all virtual ranks are enqueued on `stream`. */
+spa_status spa_ulysses_attention_local(spa_plan *plan, const void *const q[], const void *const k[],
+                                       const void *const v[], void *const out[], void *ws, void *stream);
+spa_status spa_pipesp_attention_local(spa_plan *plan, const void *const q[], const void *const k[],
+                                      const void *const v[], void *const out[], void *ws, void *stream);
+spa_status spa_aco_attention_local(spa_plan *plan, const void *const q[], const void *const k[],
+                                   const void *const v[], void *const out[], void *ws, void *stream);
+
+/* ------------------------------------------------------------------ building blocks (bit-exact tests)
+ * seq->head reshard ("all_to_all"): x [B,S/P,H,D] ->
+ * x_head [B,S,h,D] where x_head[b, p*S/P+t, j] = x_p[b, t, rank*h+j].  One stage. */
+spa_status spa_reshard_seq_to_head(spa_plan *plan, const void *x, void *x_head, void *ws, void *stream);
+/* head->seq reshard (inverse): x_head [B,S,h,D] -> x [B,S/P,H,D]. */
+spa_status spa_reshard_head_to_seq(spa_plan *plan, const void *x_head, void *x, void *ws, void *stream);
+spa_status spa_reshard_seq_to_head_local(spa_plan *plan, const void *const x[], void *const x_head[], void *ws,
+                                         void *stream);
+spa_status spa_reshard_head_to_seq_local(spa_plan *plan, const void *const x_head[], void *const x[], void *ws,
+                                         void *stream);
+
+/* Single-GPU attention kernel (tcgen05/TMEM/TMA), Alg. 1 line 3 for a group of heads:
+ *   o[b, s, j, :] = softmax_t(q[b,s,j,:] . k[b,t,j,:] / sqrt(D)) v[b,t,j,:]
+ * for b < B, s < Sq, j < n_heads, t < Skv.  Element (b, s, j, d) of q lives at
+ * q + b*q_batch_stride + s*q_tok_stride + j*D + d (strides in elements, multiples of 8);
+ * same for k, v (kv strides) and o (o strides).  D in {64, 96, 128}. */
+spa_status spa_attention_fwd(const void *q, const void *k, const void *v, void *o, int B, int Sq, int Skv,
+                             int n_heads, int D, long long q_tok_stride, long long q_batch_stride,
+                             long long kv_tok_stride, long long kv_batch_stride, long long o_tok_stride,
+                             long long o_batch_stride, void *stream);
+
+/* ------------------------------------------------------------------ host-side description (no GPU needed)
+ * Buffers: 0 q, 1 k, 2 v, 3 out (the caller's, of source rank `src`), 4 ws (of rank `rank`). */
+typedef struct {
+    int src_buf, dst_buf;           /* buffer ids above */
+    int src_rank, dst_rank;         /* whose buffer (for ws / user buffers) */
+    long long src_off, dst_off;     /* byte offsets */
+    long long count[4];             /* run index extents, outermost first */
+    long long src_stride[4], dst_stride[4]; /* byte strides per level */
+    long long run_bytes;            /* contiguous bytes per run (multiple of 64) */
+} spa_copy_desc;
+/* Messages of one stage's exchange as seen by `rank` (dir 0 = input Q/K/V, 1 = output O):
+ * peer, direction (0 send, 1 recv), buffer id (4 = this rank's ws), byte offset, bytes.
+ * For every ordered pair (p, q), p's sends to q and q's receives from p appear in the same
+ * order, which is how they are matched (NCCL semantics). */
+typedef struct {
+    int peer, is_recv, buf;
+    long long off, bytes;
+} spa_msg;
+spa_status spa_plan_describe_pack(const spa_plan *plan, int rank, spa_copy_desc *out, int max, int *n);
+spa_status spa_plan_describe_unpack(const spa_plan *plan, int rank, spa_copy_desc *out, int max, int *n);
+spa_status spa_plan_describe_messages(const spa_plan *plan, int stage, int dir, int rank, spa_msg *out, int max,
+                                      int *n);
+/* Attention problem of stage k on owner rank `rank`: ws byte offsets of Q, K, V, O and Sq, Skv, n_heads. */
+typedef struct {
+    long long q_off, k_off, v_off, o_off;
+    int B, Sq, Skv, n_heads;
+    long long q_tok_stride, q_batch_stride, kv_tok_stride, kv_batch_stride; /* elements */
+} spa_attn_desc;
+spa_status spa_plan_describe_attention(const spa_plan *plan, int stage, int rank, spa_attn_desc *out);
+
+/* ------------------------------------------------------------------ misc */
+/* pad_heads: smallest multiple of n >= H; *pad_count = that - H. */
+int spa_pad_heads(int H, int n, int *pad_count);
+const char *spa_status_string(spa_status s);
+const char *spa_last_error(void);
+/* Library version string. */
+const char *spa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPA_H_ */

@@ -1,0 +1,932 @@
+// spa_api.cpp -- rank groups, plans, the per-stage pipeline scheduler and the C ABI (include/spa.h).
+//
+// Path of one call on one rank (Alg. 1, lines 1-13):
+//   caller stream Sc: pack (seq->head send layout, all stages, one launch)
+//   comm stream   Sm: in(0), in(1), out(0), in(2), out(1), ..., out(N-1)     (fixed issue order)
+//   Sc:               attn(0), attn(1), ..., attn(N-1), unpack(+Psi_g)
+//   events: pack -> in(0); in(k) -> attn(k); attn(k) -> out(k); out(N-1) -> unpack.
+// in(k+1) and out(k-1) therefore overlap attn(k) (the paper's "record event / wait on CUDA
+// stream / All_to_All", extended to the input side, R8).
+// N_st = 1 is Ulysses.  Stage k = (head group kh, query chunk c), k = kh*C + c.
+#include "../../include/spa.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "spa_internal.h"
+
+using namespace spa;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+spa_status fail(spa_status s, const std::string &msg) {
+    g_last_error = msg;
+    return s;
+}
+#define SPA_CHECK_CUDA(expr)                                                                                   \
+    do {                                                                                                       \
+        cudaError_t _e = (expr);                                                                               \
+        if (_e != cudaSuccess)                                                                                 \
+            return fail(SPA_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));                   \
+    } while (0)
+#define SPA_CHECK_NCCL(expr)                                                                                   \
+    do {                                                                                                       \
+        ncclResult_t _r = (expr);                                                                              \
+        if (_r != ncclSuccess) return fail(SPA_ERR_COMM, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+    } while (0)
+#define SPA_TRY(expr)                       \
+    do {                                    \
+        spa_status _s = (expr);             \
+        if (_s != SPA_OK) return _s;        \
+    } while (0)
+
+enum Kind { KIND_NCCL = 0, KIND_LOOPBACK = 1, KIND_HOST = 2 };
+enum Buf { BUF_Q = 0, BUF_K = 1, BUF_V = 2, BUF_OUT = 3, BUF_WS = 4, BUF_XHEAD = 5 };
+
+long long align_up(long long x, long long a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct spa_comm {
+    int kind = KIND_HOST;
+    int nranks = 1;
+    int rank = 0;  // -1 for loopback
+    int device = 0;
+    ncclComm_t nccl = nullptr;
+    cudaStream_t stream = nullptr;  // comm stream (highest priority), created on first use
+};
+
+namespace {
+
+struct Split {
+    int G_h, C, g;
+    std::vector<int> cb;  // chunk bounds (C+1)
+    int n() const { return G_h * C; }
+};
+
+struct Ptrs {  // user buffers per source rank (loopback: arrays; NCCL: one entry)
+    std::vector<const void *> q, k, v;
+    std::vector<void *> out;
+    std::vector<void *> xhead;  // reshard targets/sources per rank
+    uint8_t *ws = nullptr;
+};
+
+}  // namespace
+
+struct spa_plan {
+    spa_comm *comm = nullptr;
+    spa_shape sh{};
+    int P = 1;      // ranks owning heads (all ranks)
+    int Psrc = 1;   // ranks holding sequence shards
+    int h = 1, S_l = 1;
+    Split split;
+    // per-rank workspace layout (bytes)
+    long long E_src = 0, E_own = 0;  // elements of one send-side / owner-side tensor
+    long long off_sendQ = 0, off_sendK = 0, off_sendV = 0, off_orecv = 0;
+    long long off_recvQ = 0, off_recvK = 0, off_recvV = 0, off_O = 0;
+    long long ws_rank_bytes = 0;
+    // options
+    bool profile = false, skip_comm = false, coproc_busy = false;
+    // runtime resources (lazy)
+    std::vector<cudaEvent_t> sync_ev;  // scheduling events (no timing)
+    std::vector<cudaEvent_t> prof_ev;  // timing events
+    spa_profile last{};
+    bool have_profile = false;
+    std::map<std::string, int> prof_idx;
+    int attn_launches = 0, copy_launches = 0;
+    cudaStream_t sc_alt = nullptr;  // second compute stream: odd stages, so stage k+1 fills stage k's wave tail
+};
+
+namespace {
+
+// ------------------------------------------------------------------ stage split (R7)
+Split make_split(int h, int S_l, int stages) {
+    Split s;
+    s.G_h = std::gcd(stages, h);
+    s.C = stages / s.G_h;
+    s.g = h / s.G_h;
+    s.cb.resize(s.C + 1);
+    for (int c = 0; c <= s.C; ++c) s.cb[c] = (int)((long long)c * S_l / s.C);
+    return s;
+}
+
+bool is_source(const spa_plan *p, int r) { return r >= 0 && r < p->Psrc; }
+
+// ------------------------------------------------------------------ offsets (elements)
+// send / orecv (source side): [kh][q][b][t][jj][d], q < P, t < S_l
+long long idx_send(const spa_plan *p, const Split &s, int kh, int q, int b, int t) {
+    return ((((long long)kh * p->P + q) * p->sh.B + b) * p->S_l + t) * s.g * p->sh.D;
+}
+// recvQ / O (owner side), stage (kh, c): [b][Psrc*L][jj][d] at base(kh,c)
+long long base_stage(const spa_plan *p, const Split &s, int kh, int c) {
+    return ((long long)kh * p->sh.B * p->sh.S + (long long)p->sh.B * p->Psrc * s.cb[c]) * s.g * p->sh.D;
+}
+long long idx_qo(const spa_plan *p, const Split &s, int kh, int c, int b, int src) {
+    const long long L = s.cb[c + 1] - s.cb[c];
+    return base_stage(p, s, kh, c) + ((long long)b * p->Psrc * L + (long long)src * L) * s.g * p->sh.D;
+}
+// recvK / recvV (owner side): [kh][b][S][jj][d]
+long long idx_kv(const spa_plan *p, const Split &s, int kh, int b, int src) {
+    return (((long long)kh * p->sh.B + b) * p->sh.S + (long long)src * p->S_l) * s.g * p->sh.D;
+}
+
+struct Msg {
+    int peer, is_recv, buf;
+    long long off, bytes;
+};
+
+// Input exchange of stage k as seen by rank r (sends first, then receives).
+// tensors: bitmask 1=Q 2=K 4=V.  q_recv_buf: BUF_WS (recvQ region) or BUF_XHEAD (reshard target).
+void gen_in_msgs(const spa_plan *p, const Split &s, int k, int r, int tensors, int q_recv_buf, std::vector<Msg> &m) {
+    const int kh = k / s.C, c = k % s.C;
+    const long long L = s.cb[c + 1] - s.cb[c];
+    const long long run = (long long)s.g * p->sh.D * 2;
+    const bool kv = (c == 0);
+    if (is_source(p, r)) {
+        for (int q = 0; q < p->P; ++q)
+            for (int b = 0; b < p->sh.B; ++b) {
+                if (tensors & 1) m.push_back({q, 0, BUF_WS, p->off_sendQ + idx_send(p, s, kh, q, b, s.cb[c]) * 2, L * run});
+                if (kv && (tensors & 2)) m.push_back({q, 0, BUF_WS, p->off_sendK + idx_send(p, s, kh, q, b, 0) * 2, p->S_l * run});
+                if (kv && (tensors & 4)) m.push_back({q, 0, BUF_WS, p->off_sendV + idx_send(p, s, kh, q, b, 0) * 2, p->S_l * run});
+            }
+    }
+    for (int src = 0; src < p->Psrc; ++src)
+        for (int b = 0; b < p->sh.B; ++b) {
+            if (tensors & 1) {
+                const long long rel = idx_qo(p, s, kh, c, b, src) * 2;
+                m.push_back({src, 1, q_recv_buf, (q_recv_buf == BUF_WS ? p->off_recvQ : 0) + rel, L * run});
+            }
+            if (kv && (tensors & 2)) m.push_back({src, 1, BUF_WS, p->off_recvK + idx_kv(p, s, kh, b, src) * 2, p->S_l * run});
+            if (kv && (tensors & 4)) m.push_back({src, 1, BUF_WS, p->off_recvV + idx_kv(p, s, kh, b, src) * 2, p->S_l * run});
+        }
+}
+
+// Output exchange of stage k as seen by rank r.  o_send_buf: BUF_WS (O region) or BUF_XHEAD.
+void gen_out_msgs(const spa_plan *p, const Split &s, int k, int r, int o_send_buf, std::vector<Msg> &m) {
+    const int kh = k / s.C, c = k % s.C;
+    const long long L = s.cb[c + 1] - s.cb[c];
+    const long long run = (long long)s.g * p->sh.D * 2;
+    for (int src = 0; src < p->Psrc; ++src)
+        for (int b = 0; b < p->sh.B; ++b) {
+            const long long rel = idx_qo(p, s, kh, c, b, src) * 2;
+            m.push_back({src, 0, o_send_buf, (o_send_buf == BUF_WS ? p->off_O : 0) + rel, L * run});
+        }
+    if (is_source(p, r)) {
+        for (int q = 0; q < p->P; ++q)
+            for (int b = 0; b < p->sh.B; ++b)
+                m.push_back({q, 1, BUF_WS, p->off_orecv + idx_send(p, s, kh, q, b, s.cb[c]) * 2, L * run});
+    }
+}
+
+// Pack (source rank): send[kh][q][b][t][jj][d] = X[b][t][q*h + kh*g + jj][d]
+CopyJob pack_job(const spa_plan *p, const Split &s, const void *x, long long dst_off, uint8_t *ws) {
+    const long long D2 = (long long)p->sh.D * 2, H = p->sh.H;
+    CopyJob j{};
+    j.src = reinterpret_cast<const uint8_t *>(x);
+    j.dst = ws + dst_off;
+    j.count[0] = s.G_h; j.count[1] = p->P; j.count[2] = p->sh.B; j.count[3] = p->S_l;
+    j.src_stride[0] = s.g * D2; j.src_stride[1] = p->h * D2; j.src_stride[2] = p->S_l * H * D2; j.src_stride[3] = H * D2;
+    const long long run = s.g * D2;
+    j.dst_stride[3] = run; j.dst_stride[2] = p->S_l * run; j.dst_stride[1] = p->sh.B * p->S_l * run;
+    j.dst_stride[0] = p->P * p->sh.B * p->S_l * run;
+    j.run_bytes = run;
+    return j;
+}
+// Unpack (source rank), Psi_g fused: out[b][t][q*h + kh*g + jj][d] = orecv[kh][q][b][t][jj][d]  (a5)
+CopyJob unpack_job(const spa_plan *p, const Split &s, uint8_t *ws, long long src_off, void *out) {
+    CopyJob j = pack_job(p, s, nullptr, 0, nullptr);
+    std::swap(j.src_stride, j.dst_stride);
+    j.src = ws + src_off;
+    j.dst = reinterpret_cast<uint8_t *>(out);
+    return j;
+}
+
+spa_copy_desc to_desc(const CopyJob &j, int sb, int sr, long long so, int db, int dr, long long dof) {
+    spa_copy_desc d{};
+    d.src_buf = sb; d.src_rank = sr; d.src_off = so; d.dst_buf = db; d.dst_rank = dr; d.dst_off = dof;
+    for (int i = 0; i < 4; ++i) { d.count[i] = j.count[i]; d.src_stride[i] = j.src_stride[i]; d.dst_stride[i] = j.dst_stride[i]; }
+    d.run_bytes = j.run_bytes;
+    return d;
+}
+
+// ------------------------------------------------------------------ runtime helpers
+spa_status ensure_stream(spa_comm *c) {
+    if (c->stream) return SPA_OK;
+    SPA_CHECK_CUDA(cudaSetDevice(c->device));
+    int lo = 0, hi = 0;
+    SPA_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    SPA_CHECK_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi));
+    return SPA_OK;
+}
+
+spa_status ensure_events(spa_plan *p, size_t n_sync, size_t n_prof) {
+    while (p->sync_ev.size() < n_sync) {
+        cudaEvent_t e;
+        SPA_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        p->sync_ev.push_back(e);
+    }
+    while (p->prof_ev.size() < n_prof) {
+        cudaEvent_t e;
+        SPA_CHECK_CUDA(cudaEventCreate(&e));
+        p->prof_ev.push_back(e);
+    }
+    return SPA_OK;
+}
+
+struct Prof {  // named timing-event pairs recorded on a stream
+    spa_plan *p;
+    int next = 0;
+    std::vector<std::pair<std::string, std::pair<int, int>>> spans;
+    std::map<std::string, int> open;
+    void begin(const std::string &name, cudaStream_t st) {
+        if (!p->profile) return;
+        int i = next++;
+        cudaEventRecord(p->prof_ev[i], st);
+        open[name] = i;
+    }
+    void end(const std::string &name, cudaStream_t st) {
+        if (!p->profile) return;
+        int i = next++;
+        cudaEventRecord(p->prof_ev[i], st);
+        spans.push_back({name, {open[name], i}});
+    }
+};
+
+struct Exec {  // everything one call needs
+    spa_plan *p;
+    const Split *s;
+    Ptrs ptr;
+    cudaStream_t sc, sm, sc_alt;
+    bool has_out = true;      // unpack at the end (false: reshard seq->head)
+    bool has_attn = true;     // attention stage (false: reshard only)
+    int in_tensors = 7;
+    int q_recv_buf = BUF_WS, o_send_buf = BUF_WS;
+    bool has_pack = true;
+};
+
+uint8_t *resolve(const Exec &x, int rank, int buf, long long off) {
+    const spa_plan *p = x.p;
+    int idx = (p->comm->kind == KIND_LOOPBACK) ? rank : 0;
+    switch (buf) {
+        case BUF_WS:
+            return x.ptr.ws + (p->comm->kind == KIND_LOOPBACK ? (long long)rank * p->ws_rank_bytes : 0) + off;
+        case BUF_XHEAD: return reinterpret_cast<uint8_t *>(x.ptr.xhead[idx]) + off;
+        case BUF_OUT: return reinterpret_cast<uint8_t *>(x.ptr.out[idx]) + off;
+        case BUF_Q: return (uint8_t *)x.ptr.q[idx] + off;
+        case BUF_K: return (uint8_t *)x.ptr.k[idx] + off;
+        default: return (uint8_t *)x.ptr.v[idx] + off;
+    }
+}
+
+// Issue one stage exchange (dir 0 in, 1 out) on the comm stream.
+spa_status run_exchange(Exec &x, int k, int dir) {
+    spa_plan *p = x.p;
+    if (p->skip_comm) return SPA_OK;
+    if (p->comm->kind == KIND_NCCL) {
+        std::vector<Msg> m;
+        if (dir == 0) gen_in_msgs(p, *x.s, k, p->comm->rank, x.in_tensors, x.q_recv_buf, m);
+        else gen_out_msgs(p, *x.s, k, p->comm->rank, x.o_send_buf, m);
+        SPA_CHECK_NCCL(ncclGroupStart());
+        for (const Msg &g : m) {
+            uint8_t *ptr = resolve(x, p->comm->rank, g.buf, g.off);
+            if (g.is_recv) SPA_CHECK_NCCL(ncclRecv(ptr, (size_t)g.bytes, ncclUint8, g.peer, p->comm->nccl, x.sm));
+            else SPA_CHECK_NCCL(ncclSend(ptr, (size_t)g.bytes, ncclUint8, g.peer, p->comm->nccl, x.sm));
+        }
+        SPA_CHECK_NCCL(ncclGroupEnd());
+        return SPA_OK;
+    }
+    // loopback: match the i-th send p->q with the i-th receive of q from p (NCCL semantics) -> copies
+    std::vector<std::vector<Msg>> per(p->P);
+    for (int r = 0; r < p->P; ++r) {
+        if (dir == 0) gen_in_msgs(p, *x.s, k, r, x.in_tensors, x.q_recv_buf, per[r]);
+        else gen_out_msgs(p, *x.s, k, r, x.o_send_buf, per[r]);
+    }
+    std::vector<CopyJob> jobs;
+    for (int src = 0; src < p->P; ++src)
+        for (int dst = 0; dst < p->P; ++dst) {
+            std::vector<const Msg *> sends, recvs;
+            for (const Msg &g : per[src]) if (!g.is_recv && g.peer == dst) sends.push_back(&g);
+            for (const Msg &g : per[dst]) if (g.is_recv && g.peer == src) recvs.push_back(&g);
+            if (sends.size() != recvs.size()) return fail(SPA_ERR_COMM, "loopback: unmatched messages");
+            for (size_t i = 0; i < sends.size(); ++i) {
+                if (sends[i]->bytes != recvs[i]->bytes) return fail(SPA_ERR_COMM, "loopback: size mismatch");
+                CopyJob j{};
+                j.src = resolve(x, src, sends[i]->buf, sends[i]->off);
+                j.dst = resolve(x, dst, recvs[i]->buf, recvs[i]->off);
+                j.count[0] = j.count[1] = j.count[2] = j.count[3] = 1;
+                j.run_bytes = sends[i]->bytes;
+                jobs.push_back(j);
+            }
+        }
+    SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sm, &p->copy_launches));
+    return SPA_OK;
+}
+
+spa_status run_attention(Exec &x, int k, cudaStream_t st) {
+    spa_plan *p = x.p;
+    const Split &s = *x.s;
+    const int kh = k / s.C, c = k % s.C;
+    const long long L = s.cb[c + 1] - s.cb[c];
+    const int nr = (p->comm->kind == KIND_LOOPBACK) ? p->P : 1;
+    for (int rr = 0; rr < nr; ++rr) {
+        const int r = (p->comm->kind == KIND_LOOPBACK) ? rr : p->comm->rank;
+        uint8_t *ws = resolve(x, r, BUF_WS, 0);
+        AttnProblem a{};
+        a.q = ws + p->off_recvQ + base_stage(p, s, kh, c) * 2;
+        a.k = ws + p->off_recvK + idx_kv(p, s, kh, 0, 0) * 2;
+        a.v = ws + p->off_recvV + idx_kv(p, s, kh, 0, 0) * 2;
+        a.o = ws + p->off_O + base_stage(p, s, kh, c) * 2;
+        a.B = p->sh.B; a.Sq = (int)(p->Psrc * L); a.Skv = p->sh.S; a.n_heads = s.g; a.D = p->sh.D;
+        a.q_tok_stride = a.kv_tok_stride = a.o_tok_stride = (long long)s.g * p->sh.D;
+        a.q_batch_stride = a.o_batch_stride = p->Psrc * L * s.g * p->sh.D;
+        a.kv_batch_stride = (long long)p->sh.S * s.g * p->sh.D;
+        SPA_CHECK_CUDA(launch_attention(a, st));
+        ++p->attn_launches;
+    }
+    return SPA_OK;
+}
+
+spa_status run_pack(Exec &x) {
+    spa_plan *p = x.p;
+    std::vector<CopyJob> jobs;
+    const int nr = (p->comm->kind == KIND_LOOPBACK) ? p->Psrc : (is_source(p, p->comm->rank) ? 1 : 0);
+    for (int i = 0; i < nr; ++i) {
+        const int r = (p->comm->kind == KIND_LOOPBACK) ? i : p->comm->rank;
+        uint8_t *ws = resolve(x, r, BUF_WS, 0);
+        if (x.in_tensors & 1) jobs.push_back(pack_job(p, *x.s, x.ptr.q[i], p->off_sendQ, ws));
+        if (x.in_tensors & 2) jobs.push_back(pack_job(p, *x.s, x.ptr.k[i], p->off_sendK, ws));
+        if (x.in_tensors & 4) jobs.push_back(pack_job(p, *x.s, x.ptr.v[i], p->off_sendV, ws));
+    }
+    if (jobs.empty()) return SPA_OK;
+    SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sc, &p->copy_launches));
+    return SPA_OK;
+}
+
+spa_status run_unpack(Exec &x) {
+    spa_plan *p = x.p;
+    std::vector<CopyJob> jobs;
+    const int nr = (p->comm->kind == KIND_LOOPBACK) ? p->Psrc : (is_source(p, p->comm->rank) ? 1 : 0);
+    for (int i = 0; i < nr; ++i) {
+        const int r = (p->comm->kind == KIND_LOOPBACK) ? i : p->comm->rank;
+        jobs.push_back(unpack_job(p, *x.s, resolve(x, r, BUF_WS, 0), p->off_orecv, x.ptr.out[i]));
+    }
+    if (jobs.empty()) return SPA_OK;
+    SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sc, &p->copy_launches));
+    return SPA_OK;
+}
+
+void finish_profile(spa_plan *p, const Prof &pr) {
+    p->have_profile = false;
+    if (!p->profile) return;
+    p->last = spa_profile{};
+    p->last.n_stages = 0;
+    p->prof_idx.clear();
+    // stored as pairs; resolved on demand in spa_plan_last_profile (after the stream completes)
+    p->prof_idx["__n"] = (int)pr.spans.size();
+    int i = 0;
+    for (auto &sp : pr.spans) {
+        p->prof_idx[sp.first + "#b"] = sp.second.first;
+        p->prof_idx[sp.first + "#e"] = sp.second.second;
+        ++i;
+    }
+    p->have_profile = true;
+}
+
+// The whole call: single-rank fast path, else the staged pipeline.
+spa_status execute(Exec &x) {
+    spa_plan *p = x.p;
+    p->attn_launches = 0;
+    p->copy_launches = 0;
+    const Split &s = *x.s;
+    const int N = s.n();
+    SPA_TRY(ensure_events(p, 4 + 3 * (size_t)N, p->profile ? 8 + 6 * (size_t)N : 0));
+    Prof pr{p};
+    if (p->P == 1) {
+        // one rank owns everything: attention straight on the caller's [B,S,H,D] buffers
+        pr.begin("total", x.sc);
+        if (x.has_attn) {
+            AttnProblem a{};
+            a.q = x.ptr.q[0]; a.k = x.ptr.k[0]; a.v = x.ptr.v[0]; a.o = x.ptr.out[0];
+            a.B = p->sh.B; a.Sq = a.Skv = p->sh.S; a.n_heads = p->sh.H; a.D = p->sh.D;
+            a.q_tok_stride = a.kv_tok_stride = a.o_tok_stride = (long long)p->sh.H * p->sh.D;
+            a.q_batch_stride = a.kv_batch_stride = a.o_batch_stride = (long long)p->sh.S * p->sh.H * p->sh.D;
+            pr.begin("attn0", x.sc);
+            SPA_CHECK_CUDA(launch_attention(a, x.sc));
+            pr.end("attn0", x.sc);
+            ++p->attn_launches;
+        } else {
+            const long long bytes = (long long)p->sh.B * p->sh.S * p->sh.H * p->sh.D * 2;
+            const void *src = x.has_out ? x.ptr.xhead[0] : x.ptr.q[0];
+            void *dst = x.has_out ? x.ptr.out[0] : x.ptr.xhead[0];
+            SPA_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, x.sc));
+        }
+        pr.end("total", x.sc);
+        finish_profile(p, pr);
+        return SPA_OK;
+    }
+    SPA_TRY(ensure_stream(p->comm));
+    x.sm = p->comm->stream;
+    if (!p->sc_alt) SPA_CHECK_CUDA(cudaStreamCreateWithFlags(&p->sc_alt, cudaStreamNonBlocking));
+    x.sc_alt = p->sc_alt;
+    cudaEvent_t *ev = p->sync_ev.data();
+    cudaEvent_t ev_entry = ev[0], ev_pack = ev[1], ev_done = ev[2];
+    cudaEvent_t *ev_in = ev + 4, *ev_attn = ev + 4 + N, *ev_out = ev + 4 + 2 * N;
+
+    pr.begin("total", x.sc);
+    SPA_CHECK_CUDA(cudaEventRecord(ev_entry, x.sc));
+    SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_entry, 0));
+    if (x.has_pack) {
+        pr.begin("pack", x.sc);
+        SPA_TRY(run_pack(x));
+        pr.end("pack", x.sc);
+    }
+    SPA_CHECK_CUDA(cudaEventRecord(ev_pack, x.sc));
+    SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_pack, 0));
+
+    auto issue_in = [&](int k) -> spa_status {
+        const std::string nm = "in" + std::to_string(k);
+        pr.begin(nm, x.sm);
+        SPA_TRY(run_exchange(x, k, 0));
+        pr.end(nm, x.sm);
+        SPA_CHECK_CUDA(cudaEventRecord(ev_in[k], x.sm));
+        return SPA_OK;
+    };
+    if (x.has_attn) {
+        SPA_TRY(issue_in(0));
+        if (N > 1) SPA_TRY(issue_in(1));
+        for (int k = 0; k < N; ++k) {
+            cudaStream_t st = (k & 1) ? x.sc_alt : x.sc;
+            SPA_CHECK_CUDA(cudaStreamWaitEvent(st, ev_in[k], 0));
+            const std::string an = "attn" + std::to_string(k);
+            pr.begin(an, st);
+            SPA_TRY(run_attention(x, k, st));
+            pr.end(an, st);
+            SPA_CHECK_CUDA(cudaEventRecord(ev_attn[k], st));
+            SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_attn[k], 0));
+            const std::string on = "out" + std::to_string(k);
+            pr.begin(on, x.sm);
+            SPA_TRY(run_exchange(x, k, 1));
+            pr.end(on, x.sm);
+            SPA_CHECK_CUDA(cudaEventRecord(ev_out[k], x.sm));
+            if (k + 2 < N) SPA_TRY(issue_in(k + 2));
+        }
+        SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_out[N - 1], 0));
+    } else if (!x.has_out) {
+        // reshard seq->head: the one input exchange only
+        SPA_TRY(issue_in(0));
+        SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_in[0], 0));
+    } else {
+        // reshard head->seq: the one output exchange only
+        pr.begin("out0", x.sm);
+        SPA_TRY(run_exchange(x, 0, 1));
+        pr.end("out0", x.sm);
+        SPA_CHECK_CUDA(cudaEventRecord(ev_out[0], x.sm));
+        SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_out[0], 0));
+    }
+    if (x.has_out) {
+        pr.begin("unpack", x.sc);
+        SPA_TRY(run_unpack(x));
+        pr.end("unpack", x.sc);
+    }
+    pr.end("total", x.sc);
+    // make the comm stream's tail visible to later work on the caller's stream
+    SPA_CHECK_CUDA(cudaEventRecord(ev_done, x.sm));
+    SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_done, 0));
+    finish_profile(p, pr);
+    return SPA_OK;
+}
+
+spa_status check_ptr(const void *ptr, const char *what) {
+    if (!ptr) return fail(SPA_ERR_INVALID, std::string(what) + " is NULL");
+    if (reinterpret_cast<uintptr_t>(ptr) % 16) return fail(SPA_ERR_INVALID, std::string(what) + " not 16-byte aligned");
+    return SPA_OK;
+}
+
+spa_status prepare(spa_plan *p, Exec &x, void *ws, void *stream, bool local) {
+    if (!p) return fail(SPA_ERR_INVALID, "plan is NULL");
+    if (p->comm->kind == KIND_HOST) return fail(SPA_ERR_UNSUPPORTED, "host-only comm cannot execute");
+    if (local != (p->comm->kind == KIND_LOOPBACK))
+        return fail(SPA_ERR_INVALID, local ? "*_local calls need a loopback plan" : "loopback plans need the *_local calls");
+    if (p->P > 1) SPA_TRY(check_ptr(ws, "ws"));
+    x.p = p;
+    x.ptr.ws = reinterpret_cast<uint8_t *>(ws);
+    x.sc = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaSetDevice(p->comm->device);
+    if (e != cudaSuccess) return fail(SPA_ERR_CUDA, cudaGetErrorString(e));
+    return SPA_OK;
+}
+
+spa_status attention_call(spa_plan *p, int nsrc_ptrs, const void *const q[], const void *const k[],
+                          const void *const v[], void *const out[], void *ws, void *stream, bool local, bool ulysses) {
+    Exec x{};
+    SPA_TRY(prepare(p, x, ws, stream, local));
+    Split one = make_split(p->h, p->S_l, 1);
+    x.s = ulysses ? &one : &p->split;
+    for (int i = 0; i < nsrc_ptrs; ++i) {
+        SPA_TRY(check_ptr(q[i], "q")); SPA_TRY(check_ptr(k[i], "k"));
+        SPA_TRY(check_ptr(v[i], "v")); SPA_TRY(check_ptr(out[i], "out"));
+        x.ptr.q.push_back(q[i]); x.ptr.k.push_back(k[i]); x.ptr.v.push_back(v[i]); x.ptr.out.push_back(out[i]);
+    }
+    return execute(x);
+}
+
+int n_local_srcs(const spa_plan *p) { return p->comm->kind == KIND_LOOPBACK ? p->Psrc : 1; }
+
+}  // namespace
+
+// ==================================================================== C ABI
+extern "C" {
+
+const char *spa_version(void) { return "spa 0.1 (sm_100a tcgen05)"; }
+
+const char *spa_status_string(spa_status s) {
+    switch (s) {
+        case SPA_OK: return "SPA_OK";
+        case SPA_ERR_INVALID: return "SPA_ERR_INVALID";
+        case SPA_ERR_SHAPE: return "SPA_ERR_SHAPE";
+        case SPA_ERR_UNSUPPORTED: return "SPA_ERR_UNSUPPORTED";
+        case SPA_ERR_CUDA: return "SPA_ERR_CUDA";
+        case SPA_ERR_COMM: return "SPA_ERR_COMM";
+        case SPA_ERR_BUSY: return "SPA_ERR_BUSY";
+    }
+    return "SPA_ERR_UNKNOWN";
+}
+
+const char *spa_last_error(void) { return g_last_error.c_str(); }
+
+int spa_pad_heads(int H, int n, int *pad_count) {
+    if (H < 1 || n < 1) {
+        if (pad_count) *pad_count = 0;
+        return -1;
+    }
+    const int hp = (H + n - 1) / n * n;
+    if (pad_count) *pad_count = hp - H;
+    return hp;
+}
+
+spa_status spa_get_unique_id(uint8_t id[128]) {
+    if (!id) return fail(SPA_ERR_INVALID, "id is NULL");
+    ncclUniqueId u;
+    SPA_CHECK_NCCL(ncclGetUniqueId(&u));
+    static_assert(sizeof(u.internal) == 128, "nccl unique id size");
+    memcpy(id, u.internal, 128);
+    return SPA_OK;
+}
+
+spa_status spa_comm_init(spa_comm **comm, const uint8_t id[128], int nranks, int rank, int device) {
+    if (!comm || !id) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SPA_ERR_INVALID, "bad rank/nranks");
+    SPA_CHECK_CUDA(cudaSetDevice(device));
+    ncclUniqueId u;
+    memcpy(u.internal, id, 128);
+    ncclComm_t nc;
+    SPA_CHECK_NCCL(ncclCommInitRank(&nc, nranks, u, rank));
+    spa_comm *c = new spa_comm;
+    c->kind = KIND_NCCL; c->nranks = nranks; c->rank = rank; c->device = device; c->nccl = nc;
+    *comm = c;
+    return SPA_OK;
+}
+
+spa_status spa_comm_init_loopback(spa_comm **comm, int nvirtual, int device) {
+    if (!comm || nvirtual < 1) return fail(SPA_ERR_INVALID, "bad loopback arguments");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return fail(SPA_ERR_CUDA, "no such CUDA device");
+    spa_comm *c = new spa_comm;
+    c->kind = KIND_LOOPBACK; c->nranks = nvirtual; c->rank = -1; c->device = device;
+    *comm = c;
+    return SPA_OK;
+}
+
+spa_status spa_comm_init_host(spa_comm **comm, int nranks, int rank) {
+    if (!comm || nranks < 1 || rank < 0 || rank >= nranks) return fail(SPA_ERR_INVALID, "bad host comm arguments");
+    spa_comm *c = new spa_comm;
+    c->kind = KIND_HOST; c->nranks = nranks; c->rank = rank;
+    *comm = c;
+    return SPA_OK;
+}
+
+spa_status spa_comm_split(spa_comm *comm, int color, int key, spa_comm **sub) {
+    if (!comm || !sub) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (comm->kind != KIND_NCCL) return fail(SPA_ERR_UNSUPPORTED, "split needs an NCCL comm");
+    ncclComm_t nc = nullptr;
+    SPA_CHECK_NCCL(ncclCommSplit(comm->nccl, color < 0 ? NCCL_SPLIT_NOCOLOR : color, key, &nc, nullptr));
+    if (color < 0 || !nc) {
+        *sub = nullptr;
+        return SPA_OK;
+    }
+    spa_comm *c = new spa_comm;
+    c->kind = KIND_NCCL; c->device = comm->device; c->nccl = nc;
+    SPA_CHECK_NCCL(ncclCommCount(nc, &c->nranks));
+    SPA_CHECK_NCCL(ncclCommUserRank(nc, &c->rank));
+    *sub = c;
+    return SPA_OK;
+}
+
+spa_status spa_comm_check(spa_comm *comm) {
+    if (!comm) return fail(SPA_ERR_INVALID, "comm is NULL");
+    if (comm->kind == KIND_NCCL) {
+        ncclResult_t a = ncclSuccess;
+        SPA_CHECK_NCCL(ncclCommGetAsyncError(comm->nccl, &a));
+        if (a != ncclSuccess && a != ncclInProgress) return fail(SPA_ERR_COMM, ncclGetErrorString(a));
+    }
+    if (comm->kind != KIND_HOST) {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(SPA_ERR_CUDA, cudaGetErrorString(e));
+    }
+    return SPA_OK;
+}
+
+spa_status spa_comm_destroy(spa_comm *comm) {
+    if (!comm) return SPA_OK;
+    if (comm->stream) cudaStreamDestroy(comm->stream);
+    if (comm->nccl) ncclCommDestroy(comm->nccl);
+    delete comm;
+    return SPA_OK;
+}
+
+spa_status spa_comm_info(const spa_comm *comm, int *nranks, int *rank, int *kind) {
+    if (!comm) return fail(SPA_ERR_INVALID, "comm is NULL");
+    if (nranks) *nranks = comm->nranks;
+    if (rank) *rank = comm->rank;
+    if (kind) *kind = comm->kind;
+    return SPA_OK;
+}
+
+spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *shape) {
+    if (!plan || !comm || !shape) return fail(SPA_ERR_INVALID, "NULL argument");
+    const spa_shape &s = *shape;
+    if (s.B < 1 || s.S < 1 || s.H < 1) return fail(SPA_ERR_SHAPE, "B, S, H must be >= 1");
+    if (s.D != 64 && s.D != 96 && s.D != 128) return fail(SPA_ERR_UNSUPPORTED, "D must be 64, 96 or 128");
+    if (s.stages < 1) return fail(SPA_ERR_SHAPE, "stages must be >= 1");
+    const int P = comm->nranks;
+    const int Psrc = s.n_src == 0 ? P : s.n_src;
+    if (Psrc < 1 || Psrc > P) return fail(SPA_ERR_SHAPE, "n_src must be in [0, nranks]");
+    if (s.S % Psrc) return fail(SPA_ERR_SHAPE, "S must be divisible by the number of source ranks");
+    if (s.H % P) return fail(SPA_ERR_SHAPE, "H must be divisible by nranks (pad heads first: spa_pad_heads)");
+    spa_plan *p = new spa_plan;
+    p->comm = comm; p->sh = s; p->P = P; p->Psrc = Psrc;
+    p->h = s.H / P; p->S_l = s.S / Psrc;
+    p->split = make_split(p->h, p->S_l, s.stages);
+    if (p->split.C > p->S_l) {
+        delete p;
+        return fail(SPA_ERR_SHAPE, "more query chunks than local tokens");
+    }
+    p->E_src = (long long)s.B * p->S_l * s.H * s.D;
+    p->E_own = (long long)s.B * s.S * p->h * s.D;
+    if (P > 1) {
+        long long off = 0;
+        auto take = [&](long long elems) { long long o = off; off = align_up(off + elems * 2, 256); return o; };
+        p->off_sendQ = take(p->E_src); p->off_sendK = take(p->E_src); p->off_sendV = take(p->E_src);
+        p->off_orecv = take(p->E_src);
+        p->off_recvQ = take(p->E_own); p->off_recvK = take(p->E_own); p->off_recvV = take(p->E_own);
+        p->off_O = take(p->E_own);
+        p->ws_rank_bytes = off;
+    }
+    *plan = p;
+    return SPA_OK;
+}
+
+spa_status spa_plan_workspace_bytes(const spa_plan *plan, size_t *bytes) {
+    if (!plan || !bytes) return fail(SPA_ERR_INVALID, "NULL argument");
+    long long per = plan->ws_rank_bytes;
+    *bytes = (size_t)(plan->comm->kind == KIND_LOOPBACK ? per * plan->P : per);
+    return SPA_OK;
+}
+
+spa_status spa_plan_stage_split(const spa_plan *plan, int *G_h, int *C, int *g) {
+    if (!plan) return fail(SPA_ERR_INVALID, "plan is NULL");
+    if (G_h) *G_h = plan->split.G_h;
+    if (C) *C = plan->split.C;
+    if (g) *g = plan->split.g;
+    return SPA_OK;
+}
+
+spa_status spa_plan_destroy(spa_plan *plan) {
+    if (!plan) return SPA_OK;
+    for (auto e : plan->sync_ev) cudaEventDestroy(e);
+    for (auto e : plan->prof_ev) cudaEventDestroy(e);
+    if (plan->sc_alt) cudaStreamDestroy(plan->sc_alt);
+    delete plan;
+    return SPA_OK;
+}
+
+spa_status spa_plan_set_option(spa_plan *plan, int option, int value) {
+    if (!plan) return fail(SPA_ERR_INVALID, "plan is NULL");
+    switch (option) {
+        case SPA_OPT_PROFILE: plan->profile = value != 0; break;
+        case SPA_OPT_SKIP_COMM: plan->skip_comm = value != 0; break;
+        case SPA_OPT_COPROC_BUSY: plan->coproc_busy = value != 0; break;
+        default: return fail(SPA_ERR_INVALID, "unknown option");
+    }
+    return SPA_OK;
+}
+
+spa_status spa_plan_last_profile(spa_plan *plan, spa_profile *out) {
+    if (!plan || !out) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (!plan->have_profile) return fail(SPA_ERR_INVALID, "no profiled call yet (set SPA_OPT_PROFILE)");
+    spa_profile r{};
+    auto span = [&](const std::string &nm, float *dst) -> spa_status {
+        auto b = plan->prof_idx.find(nm + "#b"), e = plan->prof_idx.find(nm + "#e");
+        if (b == plan->prof_idx.end() || e == plan->prof_idx.end()) return SPA_OK;
+        cudaError_t err = cudaEventElapsedTime(dst, plan->prof_ev[b->second], plan->prof_ev[e->second]);
+        if (err != cudaSuccess) return fail(SPA_ERR_CUDA, std::string("profile: ") + cudaGetErrorString(err));
+        return SPA_OK;
+    };
+    const int N = plan->P == 1 ? 1 : plan->split.n();
+    r.n_stages = N;
+    SPA_TRY(span("total", &r.total_ms));
+    SPA_TRY(span("pack", &r.pack_ms));
+    SPA_TRY(span("unpack", &r.unpack_ms));
+    for (int k = 0; k < N && k < 64; ++k) {
+        SPA_TRY(span("attn" + std::to_string(k), &r.attn_ms[k]));
+        SPA_TRY(span("in" + std::to_string(k), &r.a2a_in_ms[k]));
+        SPA_TRY(span("out" + std::to_string(k), &r.a2a_out_ms[k]));
+    }
+    r.attn_launches = plan->attn_launches;
+    r.copy_launches = plan->copy_launches;
+    *out = r;
+    return SPA_OK;
+}
+
+spa_status spa_ulysses_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out, void *ws,
+                                 void *stream) {
+    if (plan && plan->Psrc != plan->P) return fail(SPA_ERR_INVALID, "Aco plan: use spa_aco_attention");
+    return attention_call(plan, 1, &q, &k, &v, &out, ws, stream, false, true);
+}
+spa_status spa_pipesp_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out, void *ws,
+                                void *stream) {
+    if (plan && plan->Psrc != plan->P) return fail(SPA_ERR_INVALID, "Aco plan: use spa_aco_attention");
+    return attention_call(plan, 1, &q, &k, &v, &out, ws, stream, false, false);
+}
+spa_status spa_aco_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out, void *ws,
+                             void *stream) {
+    if (!plan) return fail(SPA_ERR_INVALID, "plan is NULL");
+    if (plan->Psrc == plan->P) return fail(SPA_ERR_INVALID, "not an Aco plan (n_src must be < nranks)");
+    if (plan->coproc_busy) return fail(SPA_ERR_BUSY, "co-processor group busy");
+    const bool src = plan->comm->kind == KIND_NCCL && is_source(plan, plan->comm->rank);
+    if (!src) {
+        if (q || k || v || out) return fail(SPA_ERR_INVALID, "co-processor ranks pass NULL q/k/v/out");
+        Exec x{};
+        SPA_TRY(prepare(plan, x, ws, stream, false));
+        x.s = &plan->split;
+        return execute(x);
+    }
+    return attention_call(plan, 1, &q, &k, &v, &out, ws, stream, false, false);
+}
+
+spa_status spa_ulysses_attention_local(spa_plan *plan, const void *const q[], const void *const k[],
+                                       const void *const v[], void *const out[], void *ws, void *stream) {
+    if (!plan || !q || !k || !v || !out) return fail(SPA_ERR_INVALID, "NULL argument");
+    return attention_call(plan, n_local_srcs(plan), q, k, v, out, ws, stream, true, true);
+}
+spa_status spa_pipesp_attention_local(spa_plan *plan, const void *const q[], const void *const k[],
+                                      const void *const v[], void *const out[], void *ws, void *stream) {
+    if (!plan || !q || !k || !v || !out) return fail(SPA_ERR_INVALID, "NULL argument");
+    return attention_call(plan, n_local_srcs(plan), q, k, v, out, ws, stream, true, false);
+}
+spa_status spa_aco_attention_local(spa_plan *plan, const void *const q[], const void *const k[],
+                                   const void *const v[], void *const out[], void *ws, void *stream) {
+    if (!plan || !q || !k || !v || !out) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (plan->Psrc == plan->P) return fail(SPA_ERR_INVALID, "not an Aco plan (n_src must be < nranks)");
+    if (plan->coproc_busy) return fail(SPA_ERR_BUSY, "co-processor group busy");
+    return attention_call(plan, n_local_srcs(plan), q, k, v, out, ws, stream, true, false);
+}
+
+static spa_status reshard_call(spa_plan *plan, int n, const void *const x[], void *const xh[], void *ws, void *stream,
+                               bool local, bool to_head) {
+    Exec e{};
+    SPA_TRY(prepare(plan, e, ws, stream, local));
+    if (plan->Psrc != plan->P) return fail(SPA_ERR_INVALID, "reshard needs n_src == nranks");
+    static thread_local Split one;
+    one = make_split(plan->h, plan->S_l, 1);
+    e.s = &one;
+    e.has_attn = false;
+    e.in_tensors = 1;
+    for (int i = 0; i < n; ++i) {
+        SPA_TRY(check_ptr(x[i], "x"));
+        SPA_TRY(check_ptr(xh[i], "x_head"));
+        e.ptr.xhead.push_back(xh[i]);
+        if (to_head) e.ptr.q.push_back(x[i]);
+        else e.ptr.out.push_back(const_cast<void *>(x[i]));
+    }
+    if (to_head) {
+        e.has_out = false;
+        e.q_recv_buf = BUF_XHEAD;
+    } else {
+        e.has_pack = false;
+        e.o_send_buf = BUF_XHEAD;
+    }
+    return execute(e);
+}
+
+spa_status spa_reshard_seq_to_head(spa_plan *plan, const void *x, void *x_head, void *ws, void *stream) {
+    return reshard_call(plan, 1, &x, &x_head, ws, stream, false, true);
+}
+spa_status spa_reshard_head_to_seq(spa_plan *plan, const void *x_head, void *x, void *ws, void *stream) {
+    const void *xx = x;
+    void *xh = const_cast<void *>(x_head);
+    return reshard_call(plan, 1, &xx, &xh, ws, stream, false, false);
+}
+spa_status spa_reshard_seq_to_head_local(spa_plan *plan, const void *const x[], void *const x_head[], void *ws,
+                                         void *stream) {
+    if (!plan || !x || !x_head) return fail(SPA_ERR_INVALID, "NULL argument");
+    return reshard_call(plan, plan->P, x, x_head, ws, stream, true, true);
+}
+spa_status spa_reshard_head_to_seq_local(spa_plan *plan, const void *const x_head[], void *const x[], void *ws,
+                                         void *stream) {
+    if (!plan || !x || !x_head) return fail(SPA_ERR_INVALID, "NULL argument");
+    std::vector<const void *> xx(x, x + plan->P);
+    std::vector<void *> xh(plan->P);
+    for (int i = 0; i < plan->P; ++i) xh[i] = const_cast<void *>(x_head[i]);
+    return reshard_call(plan, plan->P, xx.data(), xh.data(), ws, stream, true, false);
+}
+
+spa_status spa_attention_fwd(const void *q, const void *k, const void *v, void *o, int B, int Sq, int Skv,
+                             int n_heads, int D, long long q_tok_stride, long long q_batch_stride,
+                             long long kv_tok_stride, long long kv_batch_stride, long long o_tok_stride,
+                             long long o_batch_stride, void *stream) {
+    SPA_TRY(check_ptr(q, "q")); SPA_TRY(check_ptr(k, "k")); SPA_TRY(check_ptr(v, "v")); SPA_TRY(check_ptr(o, "o"));
+    if (D != 64 && D != 96 && D != 128) return fail(SPA_ERR_UNSUPPORTED, "D must be 64, 96 or 128");
+    if (B < 1 || Sq < 1 || Skv < 1 || n_heads < 1) return fail(SPA_ERR_SHAPE, "B, Sq, Skv, n_heads must be >= 1");
+    for (long long st : {q_tok_stride, q_batch_stride, kv_tok_stride, kv_batch_stride, o_tok_stride, o_batch_stride})
+        if (st % 8) return fail(SPA_ERR_INVALID, "strides must be multiples of 8 elements (16 bytes)");
+    if (q_tok_stride < (long long)n_heads * D || kv_tok_stride < (long long)n_heads * D ||
+        o_tok_stride < (long long)n_heads * D)
+        return fail(SPA_ERR_SHAPE, "token stride smaller than n_heads*D");
+    AttnProblem a{q, k, v, o, B, Sq, Skv, n_heads, D, q_tok_stride, q_batch_stride,
+                  kv_tok_stride, kv_batch_stride, o_tok_stride, o_batch_stride};
+    cudaError_t e = launch_attention(a, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return fail(SPA_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
+    return SPA_OK;
+}
+
+// ------------------------------------------------------------------ describe (host only)
+spa_status spa_plan_describe_pack(const spa_plan *plan, int rank, spa_copy_desc *out, int max, int *n) {
+    if (!plan || !n) return fail(SPA_ERR_INVALID, "NULL argument");
+    *n = 0;
+    if (plan->P == 1 || !is_source(plan, rank)) return SPA_OK;
+    const Split &s = plan->split;
+    const long long offs[3] = {plan->off_sendQ, plan->off_sendK, plan->off_sendV};
+    for (int t = 0; t < 3; ++t) {
+        if (*n >= max) return fail(SPA_ERR_INVALID, "describe: output too small");
+        CopyJob j = pack_job(plan, s, nullptr, 0, nullptr);
+        out[(*n)++] = to_desc(j, BUF_Q + t, rank, 0, BUF_WS, rank, offs[t]);
+    }
+    return SPA_OK;
+}
+
+spa_status spa_plan_describe_unpack(const spa_plan *plan, int rank, spa_copy_desc *out, int max, int *n) {
+    if (!plan || !n) return fail(SPA_ERR_INVALID, "NULL argument");
+    *n = 0;
+    if (plan->P == 1 || !is_source(plan, rank)) return SPA_OK;
+    if (max < 1) return fail(SPA_ERR_INVALID, "describe: output too small");
+    CopyJob j = unpack_job(plan, plan->split, nullptr, 0, nullptr);
+    out[(*n)++] = to_desc(j, BUF_WS, rank, plan->off_orecv, BUF_OUT, rank, 0);
+    return SPA_OK;
+}
+
+spa_status spa_plan_describe_messages(const spa_plan *plan, int stage, int dir, int rank, spa_msg *out, int max,
+                                      int *n) {
+    if (!plan || !n) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (stage < 0 || stage >= plan->split.n() || rank < 0 || rank >= plan->P)
+        return fail(SPA_ERR_INVALID, "bad stage/rank");
+    std::vector<Msg> m;
+    if (plan->P > 1) {
+        if (dir == 0) gen_in_msgs(plan, plan->split, stage, rank, 7, BUF_WS, m);
+        else gen_out_msgs(plan, plan->split, stage, rank, BUF_WS, m);
+    }
+    if ((int)m.size() > max) return fail(SPA_ERR_INVALID, "describe: output too small");
+    for (size_t i = 0; i < m.size(); ++i) out[i] = {m[i].peer, m[i].is_recv, m[i].buf, m[i].off, m[i].bytes};
+    *n = (int)m.size();
+    return SPA_OK;
+}
+
+spa_status spa_plan_describe_attention(const spa_plan *p, int stage, int rank, spa_attn_desc *out) {
+    if (!p || !out) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (stage < 0 || stage >= p->split.n() || rank < 0 || rank >= p->P) return fail(SPA_ERR_INVALID, "bad stage/rank");
+    const Split &s = p->split;
+    const int kh = stage / s.C, c = stage % s.C;
+    const long long L = s.cb[c + 1] - s.cb[c];
+    out->q_off = p->off_recvQ + base_stage(p, s, kh, c) * 2;
+    out->k_off = p->off_recvK + idx_kv(p, s, kh, 0, 0) * 2;
+    out->v_off = p->off_recvV + idx_kv(p, s, kh, 0, 0) * 2;
+    out->o_off = p->off_O + base_stage(p, s, kh, c) * 2;
+    out->B = p->sh.B; out->Sq = (int)(p->Psrc * L); out->Skv = p->sh.S; out->n_heads = s.g;
+    out->q_tok_stride = out->kv_tok_stride = (long long)s.g * p->sh.D;
+    out->q_batch_stride = p->Psrc * L * s.g * p->sh.D;
+    out->kv_batch_stride = (long long)p->sh.S * s.g * p->sh.D;
+    return SPA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,44 @@
+// spa_internal.h -- internal types shared by the library's translation units.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace spa {
+
+// Attention problem for one launch (a head group of one stage, or a whole single-GPU layer).
+// Element (b, s, j, d) of q is at q + b*q_batch_stride + s*q_tok_stride + j*D + d (elements).
+struct AttnProblem {
+    const void *q, *k, *v;
+    void *o;
+    int B, Sq, Skv, n_heads, D;
+    long long q_tok_stride, q_batch_stride;
+    long long kv_tok_stride, kv_batch_stride;
+    long long o_tok_stride, o_batch_stride;
+};
+
+// Kernel-side arguments (tensor maps travel separately as __grid_constant__ parameters).
+struct AttnArgs {
+    __nv_bfloat16 *O;
+    long long o_tok_stride, o_batch_stride;
+    int Sq, Skv;
+    float scale_log2;
+};
+
+cudaError_t launch_attention(const AttnProblem &p, cudaStream_t st);
+
+// Strided run copy: for (i3,i2,i1,i0) < count: copy run_bytes from
+// src + sum(i*src_stride) to dst + sum(i*dst_stride).  run_bytes % 64 == 0, 16-B aligned.
+struct CopyJob {
+    const uint8_t *src;
+    uint8_t *dst;
+    long long count[4];
+    long long src_stride[4], dst_stride[4];
+    long long run_bytes;
+};
+constexpr int kMaxCopyJobs = 32;
+// Launches ceil(n / kMaxCopyJobs) kernels; returns number launched via *launches.
+cudaError_t launch_copy_jobs(const CopyJob *jobs, int n, cudaStream_t st, int *launches);
+
+}  // namespace spa

@@ -1,0 +1,358 @@
+"""ctypes binding of libspa.so (include/spa.h): argument marshalling only.
+
+Every step of the path runs in the library's CUDA kernels / NCCL calls.  There is no
+fallback: if libspa.so is missing or fails to load, importing the functions raises.
+torch is used for device memory and streams only (tensor.data_ptr(), stream.cuda_stream).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from typing import List, Optional, Sequence
+
+from . import _build
+
+__all__ = [
+    "SpaError", "load", "header_functions", "get_unique_id", "Comm", "Plan", "Shape", "Profile",
+    "spa_attention_fwd", "spa_pipesp_attention", "spa_ulysses_attention", "spa_aco_attention",
+    "spa_pipesp_attention_local", "spa_ulysses_attention_local", "spa_aco_attention_local",
+    "spa_reshard_seq_to_head", "spa_reshard_head_to_seq", "spa_reshard_seq_to_head_local",
+    "spa_reshard_head_to_seq_local", "spa_pad_heads", "attention", "BUF_Q", "BUF_K", "BUF_V", "BUF_OUT",
+    "BUF_WS", "SPA_OPT_PROFILE", "SPA_OPT_SKIP_COMM", "SPA_OPT_COPROC_BUSY",
+]
+
+SPA_OPT_PROFILE, SPA_OPT_SKIP_COMM, SPA_OPT_COPROC_BUSY = 1, 2, 3
+BUF_Q, BUF_K, BUF_V, BUF_OUT, BUF_WS = 0, 1, 2, 3, 4
+HEADER = os.path.join(os.path.dirname(_build.HERE), "include", "spa.h")
+
+
+class SpaError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        self.status = status
+        super().__init__(f"{where}: {_status_name(status)}: {detail}")
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int), ("S", ctypes.c_int), ("H", ctypes.c_int), ("D", ctypes.c_int),
+                ("stages", ctypes.c_int), ("n_src", ctypes.c_int)]
+
+
+class Profile(ctypes.Structure):
+    _fields_ = [("n_stages", ctypes.c_int), ("total_ms", ctypes.c_float), ("pack_ms", ctypes.c_float),
+                ("unpack_ms", ctypes.c_float), ("attn_ms", ctypes.c_float * 64),
+                ("a2a_in_ms", ctypes.c_float * 64), ("a2a_out_ms", ctypes.c_float * 64),
+                ("attn_launches", ctypes.c_int), ("copy_launches", ctypes.c_int)]
+
+
+class CopyDesc(ctypes.Structure):
+    _fields_ = [("src_buf", ctypes.c_int), ("dst_buf", ctypes.c_int), ("src_rank", ctypes.c_int),
+                ("dst_rank", ctypes.c_int), ("src_off", ctypes.c_longlong), ("dst_off", ctypes.c_longlong),
+                ("count", ctypes.c_longlong * 4), ("src_stride", ctypes.c_longlong * 4),
+                ("dst_stride", ctypes.c_longlong * 4), ("run_bytes", ctypes.c_longlong)]
+
+
+class Msg(ctypes.Structure):
+    _fields_ = [("peer", ctypes.c_int), ("is_recv", ctypes.c_int), ("buf", ctypes.c_int),
+                ("off", ctypes.c_longlong), ("bytes", ctypes.c_longlong)]
+
+
+class AttnDesc(ctypes.Structure):
+    _fields_ = [("q_off", ctypes.c_longlong), ("k_off", ctypes.c_longlong), ("v_off", ctypes.c_longlong),
+                ("o_off", ctypes.c_longlong), ("B", ctypes.c_int), ("Sq", ctypes.c_int), ("Skv", ctypes.c_int),
+                ("n_heads", ctypes.c_int), ("q_tok_stride", ctypes.c_longlong),
+                ("q_batch_stride", ctypes.c_longlong), ("kv_tok_stride", ctypes.c_longlong),
+                ("kv_batch_stride", ctypes.c_longlong)]
+
+
+_lib = None
+_P = ctypes.c_void_p
+_PP = ctypes.POINTER(ctypes.c_void_p)
+_LL = ctypes.c_longlong
+
+
+def load(build_if_missing: bool = True) -> ctypes.CDLL:
+    """Load libspa.so (building it in-tree with nvcc if absent).  Raises if that fails."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    if not os.path.exists(path):
+        if not build_if_missing:
+            raise OSError(f"libspa.so not built: {path}")
+        _build.build()
+    lib = ctypes.CDLL(path)
+    i, ip = ctypes.c_int, ctypes.POINTER(ctypes.c_int)
+    sig = {
+        "spa_version": ([], ctypes.c_char_p),
+        "spa_status_string": ([i], ctypes.c_char_p),
+        "spa_last_error": ([], ctypes.c_char_p),
+        "spa_pad_heads": ([i, i, ip], i),
+        "spa_get_unique_id": ([ctypes.c_char_p], i),
+        "spa_comm_init": ([_PP, ctypes.c_char_p, i, i, i], i),
+        "spa_comm_init_loopback": ([_PP, i, i], i),
+        "spa_comm_init_host": ([_PP, i, i], i),
+        "spa_comm_split": ([_P, i, i, _PP], i),
+        "spa_comm_check": ([_P], i),
+        "spa_comm_destroy": ([_P], i),
+        "spa_comm_info": ([_P, ip, ip, ip], i),
+        "spa_plan_create": ([_PP, _P, ctypes.POINTER(Shape)], i),
+        "spa_plan_workspace_bytes": ([_P, ctypes.POINTER(ctypes.c_size_t)], i),
+        "spa_plan_stage_split": ([_P, ip, ip, ip], i),
+        "spa_plan_destroy": ([_P], i),
+        "spa_plan_set_option": ([_P, i, i], i),
+        "spa_plan_last_profile": ([_P, ctypes.POINTER(Profile)], i),
+        "spa_ulysses_attention": ([_P, _P, _P, _P, _P, _P, _P], i),
+        "spa_pipesp_attention": ([_P, _P, _P, _P, _P, _P, _P], i),
+        "spa_aco_attention": ([_P, _P, _P, _P, _P, _P, _P], i),
+        "spa_ulysses_attention_local": ([_P, _PP, _PP, _PP, _PP, _P, _P], i),
+        "spa_pipesp_attention_local": ([_P, _PP, _PP, _PP, _PP, _P, _P], i),
+        "spa_aco_attention_local": ([_P, _PP, _PP, _PP, _PP, _P, _P], i),
+        "spa_reshard_seq_to_head": ([_P, _P, _P, _P, _P], i),
+        "spa_reshard_head_to_seq": ([_P, _P, _P, _P, _P], i),
+        "spa_reshard_seq_to_head_local": ([_P, _PP, _PP, _P, _P], i),
+        "spa_reshard_head_to_seq_local": ([_P, _PP, _PP, _P, _P], i),
+        "spa_attention_fwd": ([_P, _P, _P, _P, i, i, i, i, i, _LL, _LL, _LL, _LL, _LL, _LL, _P], i),
+        "spa_plan_describe_pack": ([_P, i, ctypes.POINTER(CopyDesc), i, ip], i),
+        "spa_plan_describe_unpack": ([_P, i, ctypes.POINTER(CopyDesc), i, ip], i),
+        "spa_plan_describe_messages": ([_P, i, i, i, ctypes.POINTER(Msg), i, ip], i),
+        "spa_plan_describe_attention": ([_P, i, i, ctypes.POINTER(AttnDesc)], i),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+def header_functions() -> List[str]:
+    """Function names declared in include/spa.h."""
+    with open(HEADER) as f:
+        text = f.read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(spa_[a-z0-9_]+)\s*\(", text)))
+
+
+def _status_name(s: int) -> str:
+    try:
+        return load().spa_status_string(s).decode()
+    except Exception:  # pragma: no cover
+        return str(s)
+
+
+def _check(status: int, where: str):
+    if status != 0:
+        raise SpaError(status, where, load().spa_last_error().decode(errors="replace"))
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _arr(ptrs: Sequence) -> ctypes.Array:
+    return (ctypes.c_void_p * len(ptrs))(*[_ptr(p) for p in ptrs])
+
+
+def spa_pad_heads(H: int, n: int):
+    pad = ctypes.c_int(0)
+    hp = load().spa_pad_heads(H, n, ctypes.byref(pad))
+    return hp, pad.value
+
+
+def get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load().spa_get_unique_id(buf), "spa_get_unique_id")
+    return buf.raw
+
+
+class Comm:
+    """spa_comm wrapper.  Use Comm.nccl(...), Comm.loopback(...) or Comm.host(...)."""
+
+    def __init__(self, handle: int):
+        self.h = ctypes.c_void_p(handle)
+        n, r, k = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(load().spa_comm_info(self.h, ctypes.byref(n), ctypes.byref(r), ctypes.byref(k)), "spa_comm_info")
+        self.nranks, self.rank, self.kind = n.value, r.value, k.value
+
+    @classmethod
+    def nccl(cls, uid: bytes, nranks: int, rank: int, device: int) -> "Comm":
+        h = ctypes.c_void_p()
+        _check(load().spa_comm_init(ctypes.byref(h), uid, nranks, rank, device), "spa_comm_init")
+        return cls(h.value)
+
+    @classmethod
+    def loopback(cls, nvirtual: int, device: int = 0) -> "Comm":
+        h = ctypes.c_void_p()
+        _check(load().spa_comm_init_loopback(ctypes.byref(h), nvirtual, device), "spa_comm_init_loopback")
+        return cls(h.value)
+
+    @classmethod
+    def host(cls, nranks: int, rank: int) -> "Comm":
+        h = ctypes.c_void_p()
+        _check(load().spa_comm_init_host(ctypes.byref(h), nranks, rank), "spa_comm_init_host")
+        return cls(h.value)
+
+    def split(self, color: int, key: int) -> Optional["Comm"]:
+        h = ctypes.c_void_p()
+        _check(load().spa_comm_split(self.h, color, key, ctypes.byref(h)), "spa_comm_split")
+        return Comm(h.value) if h.value else None
+
+    def check(self):
+        _check(load().spa_comm_check(self.h), "spa_comm_check")
+
+    def close(self):
+        if self.h:
+            load().spa_comm_destroy(self.h)
+            self.h = None
+
+
+class Plan:
+    def __init__(self, comm: Comm, B: int, S: int, H: int, D: int, stages: int = 1, n_src: int = 0):
+        self.comm = comm
+        self.shape = Shape(B, S, H, D, stages, n_src)
+        h = ctypes.c_void_p()
+        _check(load().spa_plan_create(ctypes.byref(h), comm.h, ctypes.byref(self.shape)), "spa_plan_create")
+        self.h = h
+        self.B, self.S, self.H, self.D, self.stages = B, S, H, D, stages
+        self.n_src = n_src or comm.nranks
+
+    @property
+    def workspace_bytes(self) -> int:
+        n = ctypes.c_size_t()
+        _check(load().spa_plan_workspace_bytes(self.h, ctypes.byref(n)), "spa_plan_workspace_bytes")
+        return n.value
+
+    @property
+    def stage_split(self):
+        a, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(load().spa_plan_stage_split(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)),
+               "spa_plan_stage_split")
+        return a.value, b.value, c.value
+
+    def set_option(self, option: int, value: int):
+        _check(load().spa_plan_set_option(self.h, option, value), "spa_plan_set_option")
+
+    def last_profile(self) -> Profile:
+        p = Profile()
+        _check(load().spa_plan_last_profile(self.h, ctypes.byref(p)), "spa_plan_last_profile")
+        return p
+
+    def workspace(self, device="cuda"):
+        import torch
+        return torch.empty(max(self.workspace_bytes, 16), dtype=torch.uint8, device=device)
+
+    # -- host-side descriptions (no GPU needed)
+    def describe_pack(self, rank: int) -> List[CopyDesc]:
+        out = (CopyDesc * 16)()
+        n = ctypes.c_int()
+        _check(load().spa_plan_describe_pack(self.h, rank, out, 16, ctypes.byref(n)), "describe_pack")
+        return list(out[:n.value])
+
+    def describe_unpack(self, rank: int) -> List[CopyDesc]:
+        out = (CopyDesc * 16)()
+        n = ctypes.c_int()
+        _check(load().spa_plan_describe_unpack(self.h, rank, out, 16, ctypes.byref(n)), "describe_unpack")
+        return list(out[:n.value])
+
+    def describe_messages(self, stage: int, direction: int, rank: int) -> List[Msg]:
+        cap = 4 * self.comm.nranks * self.B * 3 + 16
+        out = (Msg * cap)()
+        n = ctypes.c_int()
+        _check(load().spa_plan_describe_messages(self.h, stage, direction, rank, out, cap, ctypes.byref(n)),
+               "describe_messages")
+        return list(out[:n.value])
+
+    def describe_attention(self, stage: int, rank: int) -> AttnDesc:
+        d = AttnDesc()
+        _check(load().spa_plan_describe_attention(self.h, stage, rank, ctypes.byref(d)), "describe_attention")
+        return d
+
+    def close(self):
+        if self.h:
+            load().spa_plan_destroy(self.h)
+            self.h = None
+
+
+# ------------------------------------------------------------------ calls (same names as the C ABI)
+def spa_attention_fwd(q, k, v, o, B, Sq, Skv, n_heads, D, q_tok_stride, q_batch_stride, kv_tok_stride,
+                      kv_batch_stride, o_tok_stride, o_batch_stride, stream=None):
+    _check(load().spa_attention_fwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), B, Sq, Skv, n_heads, D, q_tok_stride,
+                                    q_batch_stride, kv_tok_stride, kv_batch_stride, o_tok_stride, o_batch_stride,
+                                    _stream(stream)), "spa_attention_fwd")
+
+
+def attention(q, k, v, out=None, stream=None):
+    """Single-GPU multi-head attention on contiguous bf16 [B, S, H, D] tensors (all heads)."""
+    import torch
+    assert q.dtype == torch.bfloat16 and q.is_contiguous() and k.is_contiguous() and v.is_contiguous()
+    B, Sq, H, D = q.shape
+    Skv = k.shape[1]
+    if out is None:
+        out = torch.empty_like(q)
+    spa_attention_fwd(q, k, v, out, B, Sq, Skv, H, D, H * D, Sq * H * D, H * D, Skv * H * D, H * D, Sq * H * D,
+                      stream)
+    return out
+
+
+def spa_ulysses_attention(plan: Plan, q, k, v, out, ws, stream=None):
+    _check(load().spa_ulysses_attention(plan.h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(ws), _stream(stream)),
+           "spa_ulysses_attention")
+
+
+def spa_pipesp_attention(plan: Plan, q, k, v, out, ws, stream=None):
+    _check(load().spa_pipesp_attention(plan.h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(ws), _stream(stream)),
+           "spa_pipesp_attention")
+
+
+def spa_aco_attention(plan: Plan, q, k, v, out, ws, stream=None):
+    _check(load().spa_aco_attention(plan.h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(ws), _stream(stream)),
+           "spa_aco_attention")
+
+
+def spa_ulysses_attention_local(plan: Plan, qs, ks, vs, outs, ws, stream=None):
+    _check(load().spa_ulysses_attention_local(plan.h, _arr(qs), _arr(ks), _arr(vs), _arr(outs), _ptr(ws),
+                                              _stream(stream)), "spa_ulysses_attention_local")
+
+
+def spa_pipesp_attention_local(plan: Plan, qs, ks, vs, outs, ws, stream=None):
+    _check(load().spa_pipesp_attention_local(plan.h, _arr(qs), _arr(ks), _arr(vs), _arr(outs), _ptr(ws),
+                                             _stream(stream)), "spa_pipesp_attention_local")
+
+
+def spa_aco_attention_local(plan: Plan, qs, ks, vs, outs, ws, stream=None):
+    _check(load().spa_aco_attention_local(plan.h, _arr(qs), _arr(ks), _arr(vs), _arr(outs), _ptr(ws),
+                                          _stream(stream)), "spa_aco_attention_local")
+
+
+def spa_reshard_seq_to_head(plan: Plan, x, x_head, ws, stream=None):
+    _check(load().spa_reshard_seq_to_head(plan.h, _ptr(x), _ptr(x_head), _ptr(ws), _stream(stream)),
+           "spa_reshard_seq_to_head")
+
+
+def spa_reshard_head_to_seq(plan: Plan, x_head, x, ws, stream=None):
+    _check(load().spa_reshard_head_to_seq(plan.h, _ptr(x_head), _ptr(x), _ptr(ws), _stream(stream)),
+           "spa_reshard_head_to_seq")
+
+
+def spa_reshard_seq_to_head_local(plan: Plan, xs, x_heads, ws, stream=None):
+    _check(load().spa_reshard_seq_to_head_local(plan.h, _arr(xs), _arr(x_heads), _ptr(ws), _stream(stream)),
+           "spa_reshard_seq_to_head_local")
+
+
+def spa_reshard_head_to_seq_local(plan: Plan, x_heads, xs, ws, stream=None):
+    _check(load().spa_reshard_head_to_seq_local(plan.h, _arr(x_heads), _arr(xs), _ptr(ws), _stream(stream)),
+           "spa_reshard_head_to_seq_local")

@@ -1,0 +1,111 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/spa.h
+declares, validates shapes synchronously, and its multi-rank host logic (pack jobs,
+per-stage message lists, attention regions, Psi_g unpack) routes every element home."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_2511_12056_b200 import spa
+from tests import hostsim
+
+lib = spa.load()
+
+
+def test_exports_every_header_symbol():
+    names = spa.header_functions()
+    assert len(names) >= 30
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert b"sm_100a" in lib.spa_version()
+
+
+def test_status_strings_and_pad_heads():
+    assert lib.spa_status_string(0) == b"SPA_OK"
+    assert lib.spa_status_string(6) == b"SPA_ERR_BUSY"
+    assert spa.spa_pad_heads(24, 7) == (28, 4)
+    assert spa.spa_pad_heads(8, 4) == (8, 0)
+    assert spa.spa_pad_heads(5, 3) == (6, 1)
+
+
+@pytest.mark.parametrize("shape,err", [
+    (dict(B=1, S=256, H=4, D=80), 3),            # D unsupported
+    (dict(B=1, S=255, H=4, D=64), 2),            # S % P
+    (dict(B=1, S=256, H=3, D=64), 2),            # H % P
+    (dict(B=1, S=256, H=4, D=64, stages=0), 2),  # stages < 1
+    (dict(B=1, S=4, H=2, D=64, stages=8), 2),    # more query chunks than local tokens
+])
+def test_plan_validation(shape, err):
+    comm = spa.Comm.host(2, 0)
+    with pytest.raises(spa.SpaError) as e:
+        spa.Plan(comm, **shape)
+    assert e.value.status == err
+
+
+def test_host_comm_cannot_execute():
+    comm = spa.Comm.host(2, 1)
+    plan = spa.Plan(comm, 1, 256, 4, 64, stages=2)
+    with pytest.raises(spa.SpaError) as e:
+        spa.spa_pipesp_attention(plan, 16, 16, 16, 16, 16, stream=0)
+    assert e.value.status == 3
+
+
+def test_stage_split_and_workspace():
+    comm = spa.Comm.host(8, 0)
+    for st, exp in [(1, (1, 1, 3)), (3, (3, 1, 1)), (4, (1, 4, 3)), (24, (3, 8, 1)), (6, (3, 2, 1))]:
+        p = spa.Plan(comm, 1, 118_800, 24, 128, stages=st)
+        assert p.stage_split == exp
+        shard = 118_800 // 8 * 24 * 128 * 2
+        assert shard * 8 <= p.workspace_bytes < shard * 8 + 8 * 256
+
+
+def _labels(B, S, H, D, P, n_src=None):
+    n_src = n_src or P
+    S_l = S // n_src
+    b = np.arange(B)[:, None, None, None]
+    s = np.arange(S)[None, :, None, None]
+    k = np.arange(H)[None, None, :, None]
+    d = np.arange(D)[None, None, None, :]
+    X = ((b * 7 + s * 131 + k * 17 + d) % 65521).astype(np.uint16)
+    return [np.ascontiguousarray(X[:, r * S_l:(r + 1) * S_l]).view(np.uint8).reshape(-1) for r in range(n_src)], X
+
+
+@pytest.mark.parametrize("P,H,S,B,stages", [
+    (2, 4, 32, 1, 1), (2, 4, 32, 1, 2), (2, 4, 32, 2, 4), (4, 8, 64, 1, 2), (4, 8, 64, 1, 6),
+    (8, 24, 96, 1, 1), (8, 24, 96, 1, 3), (8, 24, 96, 1, 4), (8, 24, 96, 1, 24), (3, 6, 36, 2, 4),
+])
+def test_host_path_routes_every_element_home(P, H, S, B, stages):
+    D = 64
+    plans = [spa.Plan(spa.Comm.host(P, r), B, S, H, D, stages=stages) for r in range(P)]
+    xs, _ = _labels(B, S, H, D, P)
+    outs = hostsim.run_path(plans, xs, xs, xs)
+    for r in range(P):
+        assert np.array_equal(outs[r], xs[r]), r
+
+
+@pytest.mark.parametrize("n_src,N,H,stages", [(6, 8, 24, 1), (6, 8, 24, 3), (3, 4, 8, 2), (1, 2, 2, 1)])
+def test_host_path_aco(n_src, N, H, stages):
+    B, S, D = 1, 12 * n_src, 64
+    plans = [spa.Plan(spa.Comm.host(N, r), B, S, H, D, stages=stages, n_src=n_src) for r in range(N)]
+    xs, _ = _labels(B, S, H, D, N, n_src)
+    outs = hostsim.run_path(plans, xs, xs, xs)
+    for r in range(n_src):
+        assert np.array_equal(outs[r], xs[r])
+    # co-processors send nothing on the input side and receive nothing on the output side
+    for r in range(n_src, N):
+        assert not plans[r].describe_pack(r) and not plans[r].describe_unpack(r)
+        assert all(m.is_recv for m in plans[r].describe_messages(0, 0, r))
+        assert not any(m.is_recv for m in plans[r].describe_messages(0, 1, r))
+
+
+def test_messages_stay_inside_workspace():
+    P = 4
+    plans = [spa.Plan(spa.Comm.host(P, r), 2, 64, 8, 96, stages=4) for r in range(P)]
+    nb = plans[0].workspace_bytes
+    for r in range(P):
+        for k in range(4):
+            for d in (0, 1):
+                for m in plans[r].describe_messages(k, d, r):
+                    assert 0 <= m.off and m.off + m.bytes <= nb and m.off % 16 == 0 and m.bytes % 64 == 0
+            a = plans[r].describe_attention(k, r)
+            assert a.q_off % 16 == 0 and a.o_off % 16 == 0 and a.Skv == 64

@@ -1,0 +1,89 @@
+"""tcgen05 attention kernel (spa_attention_fwd through the C ABI) vs the fp64 oracle."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2511_12056_b200 import spa
+from tests import gpu_util as U
+
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(600)]
+
+
+def _run(q, k, v):
+    torch.cuda.synchronize()
+    out = spa.attention(q, k, v)
+    torch.cuda.synchronize()
+    return out
+
+
+def test_tiny_config_full():
+    """BASELINE configs[0]: B=1, S=256, H=4, D=64 -- every output element."""
+    q, k, v = U.qkv(1, 256, 4, 64)
+    U.assert_close(_run(q, k, v), U.oracle_mha(q, k, v))
+
+
+@pytest.mark.parametrize("D", [64, 96, 128])
+@pytest.mark.parametrize("S", [128, 300, 1000])
+def test_shapes_and_ragged_tails(D, S):
+    q, k, v = U.qkv(2, S, 2, D, seed=S + D)
+    U.assert_close(_run(q, k, v), U.oracle_mha(q, k, v))
+
+
+@pytest.mark.parametrize("dist", ["D1", "D4"])
+@pytest.mark.parametrize("D", [96, 128])
+def test_distributions(dist, D):
+    q, k, v = U.qkv(1, 700, 2, D, seed=3, dist=dist)
+    U.assert_close(_run(q, k, v), U.oracle_mha(q, k, v))
+
+
+def test_zero_query_is_mean_of_v():
+    q, k, v = U.qkv(1, 777, 2, 128, dist="D2")
+    out = _run(q, k, v).double().cpu()
+    mean = v.double().cpu().mean(dim=1, keepdim=True).expand_as(out)
+    assert (out - mean).abs().max().item() < 2e-3
+
+
+def test_v_one_gives_one():
+    q, k, v = U.qkv(1, 513, 3, 96, dist="D3")
+    out = _run(q, k, v).double().cpu()
+    assert (out - 1).abs().max().item() <= 2 ** -7
+
+
+def test_single_key():
+    q, k, v = U.qkv(1, 1, 2, 64)
+    out = _run(q, k, v)
+    assert torch.equal(out.view(torch.int16), v.view(torch.int16))
+
+
+def test_sq_ne_skv_and_strided_views():
+    """Separate query / key lengths and head sub-ranges through explicit strides."""
+    B, Sq, Skv, H, D = 2, 200, 450, 4, 128
+    q = U.qkv(B, Sq, H, D, seed=11)[0]
+    _, k, v = U.qkv(B, Skv, H, D, seed=12)
+    out = torch.zeros_like(q)
+    # heads 1..2 only, through strides of the full [B,S,H,D] tensors
+    spa.spa_attention_fwd(q[:, :, 1:], k[:, :, 1:], v[:, :, 1:], out[:, :, 1:], B, Sq, Skv, 2, D,
+                          H * D, Sq * H * D, H * D, Skv * H * D, H * D, Sq * H * D)
+    torch.cuda.synchronize()
+    ref = U.oracle_mha(q[:, :, 1:3].contiguous(), k[:, :, 1:3].contiguous(), v[:, :, 1:3].contiguous())
+    U.assert_close(out[:, :, 1:3], ref)
+    assert (out[:, :, 0] == 0).all() and (out[:, :, 3] == 0).all()
+
+
+def test_deterministic_and_row_independent():
+    """Bit-identical across runs, and a row's output does not depend on which tile it sits in."""
+    q, k, v = U.qkv(1, 1111, 2, 128, seed=5)
+    a = _run(q, k, v)
+    b = _run(q, k, v)
+    assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    for off in (1, 77, 300):
+        sub = _run(q[:, off:].contiguous(), k, v)
+        assert torch.equal(sub.view(torch.int16), a[:, off:].contiguous().view(torch.int16)), off
+
+
+def test_bad_arguments_raise():
+    q, k, v = U.qkv(1, 64, 1, 64)
+    with pytest.raises(spa.SpaError):
+        spa.spa_attention_fwd(q, k, v, q, 1, 64, 64, 1, 80, 80, 64 * 80, 80, 64 * 80, 80, 64 * 80)
+    with pytest.raises(spa.SpaError):
+        spa.spa_attention_fwd(q, k, v, None, 1, 64, 64, 1, 64, 64, 4096, 64, 4096, 64, 4096)
