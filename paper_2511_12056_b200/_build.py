@@ -14,6 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libspa.so")
+TRACE_LIB = os.path.join(LIBDIR, "libspa_trace.so")
 SOURCES = ["attn_fwd.cu", "reshard.cu", "spa_api.cpp"]
 HEADERS = ["ptx.cuh", "spa_internal.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -44,16 +45,20 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """trace=True builds lib/libspa_trace.so with the attention timeline hooks (tools/attn_trace.py)."""
+    out_lib = TRACE_LIB if trace else LIB
+    if not force and not trace and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     inc, lib = nccl_dirs()
     objs = []
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
               f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}", "-Xptxas", "-v" if verbose else "-O3"]
+    if trace:
+        common = common + ["-DSPA_ATTN_TRACE"]
     for src in SOURCES:
-        obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + ".o")
+        obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + (".trace.o" if trace else ".o"))
         cmd = common + ["-x", "cu" if src.endswith(".cu") else "c++", "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cpp"):
             cmd = [nvcc(), "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O3", f"-I{inc}",
@@ -65,15 +70,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(obj)
-    link = [nvcc(), *ARCH, "-shared", "-o", LIB + ".tmp", *objs, f"-L{lib}", "-l:libnccl.so.2",
+    link = [nvcc(), *ARCH, "-shared", "-o", out_lib + ".tmp", *objs, f"-L{lib}", "-l:libnccl.so.2",
             f"-Xlinker=-rpath={lib}", "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out_lib + ".tmp", out_lib)
+    return out_lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

@@ -76,7 +76,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
+    path = os.environ.get("SPA_LIB") or _build.LIB   # SPA_LIB: debug builds (lib/libspa_trace.so)
     if not os.path.exists(path):
         if not build_if_missing:
             raise OSError(f"libspa.so not built: {path}")
