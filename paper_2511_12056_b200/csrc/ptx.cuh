@@ -216,3 +216,144 @@ __device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
 }
 }  // namespace ptx
 }  // namespace spa
+
+namespace spa {
+namespace ptx {
+// 16 consecutive 32-bit TMEM columns of this thread's lane.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+// Named barrier over `nthreads` threads (multiple of 32); id 0 is __syncthreads.
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+}  // namespace ptx
+}  // namespace spa
+
+namespace spa {
+namespace ptx {
+// ------------------------------------------------------------------ clusters
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load delivered to the same smem offset (data and mbarrier complete_tx) in every CTA of cta_mask.
+__device__ __forceinline__ void tma_load_4d_mc(const CUtensorMap *m, uint64_t *bar, void *dst, int c0, int c1, int c2,
+                                               int c3, uint16_t cta_mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster."
+        "L2::cache_hint [%0], [%1, {%4, %5, %6, %7}], [%2], %3, %8;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "h"(cta_mask), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "l"(policy)
+        : "memory");
+}
+// tcgen05.commit arriving on the mbarrier at the same smem offset in every CTA of cta_mask.
+__device__ __forceinline__ void mma_commit_mc(uint64_t *bar, uint16_t cta_mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(cta_mask)
+        : "memory");
+}
+}  // namespace ptx
+}  // namespace spa
+
+namespace spa {
+namespace ptx {
+// One lane of the (converged) warp returns true (elect.sync).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\t"
+        "elect.sync r|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+}  // namespace ptx
+}  // namespace spa
+
+namespace spa {
+namespace ptx {
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+// N (multiple of 8, <= 64) consecutive columns, without waiting (no pointer casts: keeps r in registers).
+template <int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
+    static_assert(N % 8 == 0 && N <= 64, "columns");
+#pragma unroll
+    for (int c = 0; c + 32 <= N; c += 32) {
+        uint32_t t[32];
+        tmem_ld32(taddr + c, t);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[c + i] = t[i];
+    }
+    constexpr int c16 = (N / 32) * 32;
+    if ((N - c16) >= 16) {
+        uint32_t t[16];
+        tmem_ld16(taddr + c16, t);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) r[c16 + i] = t[i];
+    }
+    constexpr int c8 = c16 + ((N - c16) >= 16 ? 16 : 0);
+    if ((N - c8) >= 8) {
+        uint32_t t[8];
+        tmem_ld8(taddr + c8, t);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[c8 + i] = t[i];
+    }
+}
+template <int N>
+__device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t (&r)[N]) {
+    static_assert(N % 8 == 0 && N <= 64, "columns");
+#pragma unroll
+    for (int c = 0; c + 32 <= N; c += 32) {
+        uint32_t t[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) t[i] = r[c + i];
+        tmem_st32(taddr + c, t);
+    }
+    constexpr int c16 = (N / 32) * 32;
+    if ((N - c16) >= 16) {
+        uint32_t t[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) t[i] = r[c16 + i];
+        tmem_st16(taddr + c16, t);
+    }
+    constexpr int c8 = c16 + ((N - c16) >= 16 ? 16 : 0);
+    if ((N - c8) >= 8) {
+        uint32_t t[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t[i] = r[c8 + i];
+        tmem_st8(taddr + c8, t);
+    }
+}
+}  // namespace ptx
+}  // namespace spa

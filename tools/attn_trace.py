@@ -3,9 +3,9 @@
 
     SPA_LIB=paper_2511_12056_b200/lib/libspa_trace.so python tools/attn_trace.py [--D 128]
 Events (clock64 cycles) per KV iteration j of CTA (0,0,0):
-  0 MMA: before waiting P0(j)   1 MMA: P0(j) ready (PV0 issue)   2 MMA: P1(j) ready (PV1 issue)
-  3/8 softmax t0/t1: before S wait   4/9 S ready   5/10 S in registers   6/11 exps done   7/12 P signalled
-  14/15 producer: K_j / V_j slot free
+  0/1  MMA issuer: P(j) key-half 0/1 ready (PV half issued)
+  3/8  softmax key-half 0/1 (quarter-0 warp): before waiting for S(j)
+  4/9  S(j) ready     5/10 row max exchanged     6/11 P half written and released
 """
 import argparse
 import ctypes
@@ -36,16 +36,16 @@ assert lib.spa_debug_read_trace(ctypes.addressof(buf)) == 0
 T = np.frombuffer(buf, dtype=np.uint64).reshape(256, 16).astype(np.int64)
 t0 = T[0, 3]
 n = min(256, (args.S + 127) // 128)
-print("j  | mma0:kv-ok P0a-rdy  mma1:P1a-rdy | s0: wait  rdy  ld  exp  sig | s1: wait rdy  ld  exp  sig | kfree vfree")
-for j in list(range(0, 12)) + list(range(n // 2, n // 2 + 6)) + list(range(n - 4, n)):
+print("  j | mma: P0rdy   P1rdy | sm0: wait  Srdy   maxx   Pdone | sm1: wait  Srdy   maxx   Pdone")
+for j in list(range(0, 8)) + list(range(n // 2, n // 2 + 4)) + list(range(n - 3, n)):
     r = T[j] - t0
-    print(f"{j:3d}| {r[0]:8d} {r[1]:8d} {r[2]:8d} | {r[3]:8d} {r[4]:8d} {r[5]:8d} {r[6]:8d} {r[7]:8d} |"
-          f" {r[8]:8d} {r[9]:8d} {r[10]:8d} {r[11]:8d} {r[12]:8d} | {r[14]:8d} {r[15]:8d}")
+    print(f"{j:3d} | {r[0]:8d} {r[1]:8d} | {r[3]:8d} {r[4]:8d} {r[5]:8d} {r[6]:8d} | {r[8]:8d} {r[9]:8d} {r[10]:8d} {r[11]:8d}"
+          f" | qk: acq {r[12]:8d} got {r[13]:8d} | V: acq {r[14]:8d} got {r[15]:8d} | load K {r[2]:8d} V {r[7]:8d}")
 mid = slice(n // 4, 3 * n // 4)
-per = np.diff(T[mid, 1]).mean()
-print(f"steady-state period (P0 ready to P0 ready): {per:.0f} cycles (ideal MMA-bound 2048 at D=128)")
-for t, base in ((0, 3), (1, 8)):
-    d = T[mid]
-    print(f"tile{t}: wait S {np.mean(d[:, base+1]-d[:, base]):.0f}  ld {np.mean(d[:, base+2]-d[:, base+1]):.0f}  "
-          f"max+exp {np.mean(d[:, base+3]-d[:, base+2]):.0f}  st+sig {np.mean(d[:, base+4]-d[:, base+3]):.0f}")
-print(f"MMA wait for P0: {np.mean(T[mid,1]-T[mid,0]):.0f}   P0->P1: {np.mean(T[mid,2]-T[mid,1]):.0f}")
+d = T[mid]
+per = np.diff(d[:, 1]).mean()
+ideal = {128: 1024, 96: 768, 64: 512}[args.D]
+print(f"steady-state period per KV tile: {per:.0f} cycles (MMA-bound ideal {ideal} at D={args.D})")
+for h, base in ((0, 3), (1, 8)):
+    print(f"half{h}: wait S {np.mean(d[:, base+1]-d[:, base]):.0f}  ld+max+xchg {np.mean(d[:, base+2]-d[:, base+1]):.0f}  "
+          f"exp+store {np.mean(d[:, base+3]-d[:, base+2]):.0f}")
