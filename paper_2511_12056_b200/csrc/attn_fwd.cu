@@ -5,26 +5,25 @@
 // which is Alg. 1 line 3 `attention(Q[:,j],K[:,j],V[:,j])` for a
 // group of heads; the scale 1/sqrt(D) is the north star's (R1).
 //
-// Design (DESIGN.md §Kernels / attention), one CTA = one 128-row query tile of one (b, head):
-//   warps 0..7   softmax / correction / epilogue: warp w owns TMEM lanes 32*(w%4)..+31 (rows) and
-//                key half hf = w/4 of every 128-key tile, so each row is served by two warps on the
-//                same SM sub-partition (latency hiding) that exchange partial row maxima.
-//   warp 8       TMA producer: Q once, then K/V tiles through an NS-slot shared-memory ring in the
-//                order the MMA consumes them (K0, K1, V0, K2, V1, K3, ...); clusters of 2 CTAs
-//                (adjacent query tiles) fetch half of every K/V tile each and multicast it.
-//   warp 9       TMEM allocator + tcgen05.mma issuer (one elected lane; highest warp id = priority)
+// Design (DESIGN.md §Kernels / attention), one CTA = one 128-row query tile of one (b, head); clusters of
+// two CTAs (adjacent query tiles of the same head) share every K/V tile through TMA multicast:
+//   warps 0..15  softmax / correction / epilogue: warp w owns TMEM lanes 32*(w%4)..+31 (its rows, = its SM
+//                sub-partition) and keys [32*(w/4), 32*(w/4)+32) of every 128-key tile; the 4 warps of a row
+//                quarter assemble the row max through shared memory (named barrier) every tile.
+//   warp 16      TMA producer: Q once, then K/V tiles through an NS-slot shared-memory ring in the order the
+//                MMA consumes them (K0, K1, V0, K2, V1, K3, ...); each CTA fetches 64 of the 128 rows of every
+//                tile and multicasts them to both CTAs of the pair.
+//   warp 17      TMEM allocator + tcgen05.mma issuer (one elected lane; highest warp id = scheduling priority).
 //   TMEM: S double buffer at columns [0,128) and [128,256) (fp32), O at [256, 256+D).
-//   * S(j) = Q K_j^T   tcgen05.mma SS, M=128 N=128, into S buffer j%2 -> the MMA for S(j+1) runs
-//     while the softmax of S(j) is in progress (no MMA <-> softmax serialisation).
-//   * P(j) (bf16) is written by the softmax warps into the S buffer it came from, key half 0 over
-//     columns [0,32), half 1 over [64,96) (each warp only overwrites scores it has already read);
-//     each half is released to the MMA issuer on its own.
+//   * S(j) = Q K_j^T   tcgen05.mma SS, M=128 N=128 into S buffer j%2, so QK^T of tile j+1 runs while the
+//     softmax of tile j is in progress.
+//   * P(j) (bf16) is written by each softmax warp over the first 16 columns of its own 32 score columns (scores
+//     it has already read); key half 0 (keys 0..63) and half 1 are released to the MMA issuer separately.
 //   * O += P(j) V_j     tcgen05.mma TS (A = P from TMEM, B = V MN-major, N = D in one instruction).
-//   * online softmax in fp32, base 2 with log2(e)/sqrt(D) folded into one FFMA; the running max only
-//     moves when it grows by more than 2^8 (conditional rescale; exact, since the final 1/l uses the
-//     same max).  The decision is per row, so a row's result does not depend on the other rows of its
-//     tile (bit-identical across stage splits).  3/8 of the exponentials run as a degree-3 polynomial
-//     on the FMA pipe, the rest on MUFU.
+//   * online softmax in fp32, base 2 with log2(e)/sqrt(D) folded into one FFMA2; the running max only moves
+//     when it grows by more than 2^8 (conditional rescale; exact, since the final 1/l uses the same max).  The
+//     decision is per row, so a row's result does not depend on the other rows of its tile (bit-identical
+//     across stage splits).  A quarter of the exponentials run as a degree-3 polynomial on the FMA pipe.
 //   * keys >= Skv (ragged tail, TMA zero-filled) get score -inf; query rows >= Sq are not stored.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -91,7 +90,13 @@ struct Cfg {
     // tcgen05.ld/st of O is a 32-column-aligned x32 access.
     static constexpr int DW = 32;
     static constexpr int NSLICE = D / 32;
-    static constexpr int POLY_FROM = 4;                  // columns with (i & 7) >= 4 (1/2) use the polynomial
+    // exp2 split: key pairs with (i & 7) >= POLY_FROM use the FMA-pipe polynomial, the rest MUFU.EX2.
+    // 6 = 1/4 polynomial was fastest at D = 64, 96 and 128 (sweep of 2/4/6/8 on B200).
+#ifdef SPA_POLY_FROM
+    static constexpr int POLY_FROM = SPA_POLY_FROM;
+#else
+    static constexpr int POLY_FROM = 6;
+#endif
     static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 };
 
@@ -444,22 +449,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const long long srow = (long long)qtile * BM + row;
         const bool valid = srow < args.Sq;      // tcgen05.ld is warp-collective: every lane loads, valid lanes store
         if (kq < C::NSLICE) {   // warps kq >= D/32 own no O slice (D = 64 / 96)
-        uint32_t r[C::DW];
-        ptx::tmem_ld_cols<C::DW>(tO, r);
-        ptx::tmem_wait_ld();
-        if (valid) {
-            uint4 *dst = reinterpret_cast<uint4 *>(args.O + (long long)b * args.o_batch_stride +
-                                                   srow * args.o_tok_stride + (long long)head * D + kq * C::DW);
+            uint32_t r[C::DW];
+            ptx::tmem_ld_cols<C::DW>(tO, r);
+            ptx::tmem_wait_ld();
+            if (valid) {
+                uint4 *dst = reinterpret_cast<uint4 *>(args.O + (long long)b * args.o_batch_stride +
+                                                       srow * args.o_tok_stride + (long long)head * D + kq * C::DW);
 #pragma unroll
-            for (int v = 0; v < C::DW / 8; ++v) {
-                uint32_t w[4];
+                for (int v = 0; v < C::DW / 8; ++v) {
+                    uint32_t w[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    w[u] = ptx::pack_bf16x2(__uint_as_float(r[8 * v + 2 * u]) * inv_l,
-                                            __uint_as_float(r[8 * v + 2 * u + 1]) * inv_l);
-                dst[v] = make_uint4(w[0], w[1], w[2], w[3]);
+                    for (int u = 0; u < 4; ++u)
+                        w[u] = ptx::pack_bf16x2(__uint_as_float(r[8 * v + 2 * u]) * inv_l,
+                                                __uint_as_float(r[8 * v + 2 * u + 1]) * inv_l);
+                    dst[v] = make_uint4(w[0], w[1], w[2], w[3]);
+                }
             }
-        }
         }
     }
     ptx::tc_fence_before();
