@@ -32,7 +32,7 @@ METRIC = "ms per SP attention layer and TFLOP/s at 1/2/4/8 B200; exposed all-to-
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="osp480p93f")
@@ -65,55 +65,48 @@ def attn_flops(B, S, H, D):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled every 20 ms DURING the timed region (NVML; nvidia-smi fallback)."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
-        self.proc = None
-        self.lines = []
+    def __init__(self, gpu_index: int, period_s: float = 0.02):
+        self.gpu, self.period = gpu_index, period_s
+        self.sm, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+
+    def _loop(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            while not self._stop.is_set():
+                self.sm.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                bits = get_reasons(h)
+                for bit, name in self.REASONS.items():
+                    if bits & bit:
+                        self.reasons.add(name)
+                self._stop.wait(self.period)
+        except Exception as e:  # pragma: no cover
+            self.error = str(e)[:120]
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
+        self._t = threading.Thread(target=self._loop, daemon=True)
+        self._t.start()
+        time.sleep(0.05)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 20 ms, timed region"}
 
 
 # ------------------------------------------------------------------ CPU oracle timing
@@ -128,22 +121,29 @@ def time_oracle(S, D, rows_target_s: float, seed=0):
     K = synthgen.gen_head_rows(seed, synthgen.TENSOR_K, shape, 0, 0).double().numpy()
     V = synthgen.gen_head_rows(seed, synthgen.TENSOR_V, shape, 0, 0).double().numpy()
     nthreads = os.cpu_count() or 1
-    probe = max(nthreads, 16)
-    Q = synthgen.gen_head_rows(seed, synthgen.TENSOR_Q, shape, 0, 0, tokens=torch.arange(probe)).double().numpy()
-    t0 = time.perf_counter()
-    oracle.attention_rows(Q, K, V, nthreads)
-    dt = time.perf_counter() - t0
-    R = int(max(probe, min(65536, probe * rows_target_s / max(dt, 1e-6))))
-    R = (R // nthreads) * nthreads or nthreads
-    rows = torch.arange(R) % S
-    Q = synthgen.gen_head_rows(seed, synthgen.TENSOR_Q, shape, 0, 0, tokens=rows).double().numpy()
-    t0 = time.perf_counter()
-    oracle.attention_rows(Q, K, V, nthreads)
-    dt = time.perf_counter() - t0
+    # calibrate: grow the probe until it takes >= 1 s, then scale to the target duration
+    R = nthreads
+    while True:
+        rows = torch.arange(R) % S
+        Q = synthgen.gen_head_rows(seed, synthgen.TENSOR_Q, shape, 0, 0, tokens=rows).double().numpy()
+        t0 = time.perf_counter()
+        oracle.attention_rows(Q, K, V, nthreads)
+        dt = time.perf_counter() - t0
+        if dt >= 1.0 or R >= 1 << 20:
+            break
+        R *= 4
+    if dt < rows_target_s:
+        R = int(R * rows_target_s / dt) // nthreads * nthreads
+        rows = torch.arange(R) % S
+        Q = synthgen.gen_head_rows(seed, synthgen.TENSOR_Q, shape, 0, 0, tokens=rows).double().numpy()
+        t0 = time.perf_counter()
+        oracle.attention_rows(Q, K, V, nthreads)
+        dt = time.perf_counter() - t0
     flops = 4.0 * S * D * R
     return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": nthreads, "kind": "oracle",
-            "sample": f"{R} query rows x 1 head, full S={S} keys, D={D}, fp64 C oracle, {dt:.1f} s "
-                      f"(full layer extrapolates x{1.0:.0f} per row)", "seconds": dt, "rows": R}
+            "sample": f"{R} query rows of one head (each against all S={S} keys, D={D}), fp64 C oracle, "
+                      f"{dt:.1f} s on {nthreads} threads; per-row work is identical, so TFLOP/s carries over "
+                      f"to the full layer", "seconds": dt, "rows": R}
 
 
 def run_reference(args):
@@ -152,14 +152,28 @@ def run_reference(args):
     if rank != 0:
         return
     P = args.gpus
-    res_steps = []
-    per_step_target = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    import torch
+
+    import oracle
+    import synthgen
+    # each step = the oracle on R query rows of one head against the full K/V (bounded sample of the
+    # workload); R calibrated once so that warmup + steps take about 2.5 minutes
+    per_step_target = max(0.5, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    cal = time_oracle(S, D, per_step_target)
+    R, nthreads = cal["rows"], cal["cores"]
+    shape = (1, S, 1, D)
+    K = synthgen.gen_head_rows(0, synthgen.TENSOR_K, shape, 0, 0).double().numpy()
+    V = synthgen.gen_head_rows(0, synthgen.TENSOR_V, shape, 0, 0).double().numpy()
+    Q = synthgen.gen_head_rows(0, synthgen.TENSOR_Q, shape, 0, 0, tokens=torch.arange(R) % S).double().numpy()
+    secs = []
     for i in range(args.warmup + args.steps):
-        r = time_oracle(S, D, per_step_target, seed=i)
+        t0 = time.perf_counter()
+        oracle.attention_rows(Q, K, V, nthreads)
         if i >= args.warmup:
-            res_steps.append(r)
-    flops = sum(4.0 * S * D * r["rows"] for r in res_steps)
-    secs = sum(r["seconds"] for r in res_steps)
+            secs.append(time.perf_counter() - t0)
+    res_steps = [{"rows": R, "cores": nthreads}]
+    flops = 4.0 * S * D * R * len(secs)
+    secs = sum(secs)
     value = flops / secs / 1e12
     full_layer_s = attn_flops(B, S, H, D) / (value * 1e12)
     line = {

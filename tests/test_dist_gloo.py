@@ -1,0 +1,104 @@
+"""Multi-process check of the library's NCCL-path host logic over gloo (CPU, world_size 2).
+
+Each process plays one rank: it builds the plan on a host-only comm (same plan as the NCCL path),
+runs the described pack jobs, exchanges exactly the described per-stage messages with the other
+process through torch.distributed (gloo) point-to-point, applies an identity "attention" to the
+described regions, runs the output exchange and the described unpack (Psi_g).  The output must
+equal the input element for element, for every stage split and for Aco (1 source + 1 co-processor).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _exchange(plan, stage, direction, rank, ws):
+    from paper_2511_12056_b200 import spa
+    msgs = plan.describe_messages(stage, direction, rank)
+    reqs, counters = [], {}
+    recv_bufs = []
+    for m in msgs:
+        assert m.buf == spa.BUF_WS
+        key = (m.peer, m.is_recv)
+        tag = counters.get(key, 0)
+        counters[key] = tag + 1
+        if m.peer == rank:
+            continue
+        if m.is_recv:
+            t = torch.empty(m.bytes, dtype=torch.uint8)
+            reqs.append(dist.irecv(t, src=m.peer, tag=tag))
+            recv_bufs.append((t, m.off))
+        else:
+            reqs.append(dist.isend(torch.from_numpy(ws[m.off:m.off + m.bytes].copy()), dst=m.peer, tag=tag))
+    # self messages: i-th send to self matches i-th receive from self
+    sends = [m for m in msgs if m.peer == rank and not m.is_recv]
+    recvs = [m for m in msgs if m.peer == rank and m.is_recv]
+    assert len(sends) == len(recvs)
+    for s, r in zip(sends, recvs):
+        ws[r.off:r.off + r.bytes] = ws[s.off:s.off + s.bytes]
+    for q in reqs:
+        q.wait()
+    for t, off in recv_bufs:
+        ws[off:off + t.numel()] = t.numpy()
+
+
+def _worker(rank, world, port, cases, result):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2511_12056_b200 import spa
+    from tests import hostsim
+    ok = True
+    for (B, S, H, D, stages, n_src) in cases:
+        plan = spa.Plan(spa.Comm.host(world, rank), B, S, H, D, stages=stages, n_src=n_src)
+        nsrc = n_src or world
+        S_l = S // nsrc
+        X = ((np.arange(B * S * H * D) * 2654435761) % 65521).astype(np.uint16).reshape(B, S, H, D)
+        ws = np.zeros(plan.workspace_bytes, dtype=np.uint8)
+        x = None
+        if rank < nsrc:
+            x = np.ascontiguousarray(X[:, rank * S_l:(rank + 1) * S_l]).view(np.uint8).reshape(-1)
+            for d in plan.describe_pack(rank):
+                hostsim.run_copy(d, x, ws)
+        G_h, C, g = plan.stage_split
+        for k in range(G_h * C):
+            _exchange(plan, k, 0, rank, ws)
+            hostsim.identity_attention(plan, k, rank, ws)
+            _exchange(plan, k, 1, rank, ws)
+        if rank < nsrc:
+            out = np.zeros_like(x)
+            for d in plan.describe_unpack(rank):
+                hostsim.run_copy(d, ws, out)
+            ok &= bool(np.array_equal(out, x))
+        plan.close()
+    result[rank] = int(ok)
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_process_gloo_exchange():
+    cases = [(1, 64, 4, 64, 1, 0), (1, 64, 4, 64, 2, 0), (2, 64, 4, 96, 4, 0), (1, 128, 8, 128, 8, 0),
+             (1, 96, 6, 64, 6, 0), (1, 48, 2, 64, 1, 1), (2, 48, 4, 64, 2, 1)]
+    world = 2
+    ctx = mp.get_context("spawn")
+    result = ctx.Array("i", [0] * world)
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, result)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    assert list(result) == [1] * world
