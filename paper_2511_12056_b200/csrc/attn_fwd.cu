@@ -82,9 +82,9 @@ struct Cfg {
     static constexpr int TILE_BYTES = BM * D * 2;
     static constexpr int NS = (D == 128) ? 5 : 8;         // K/V ring slots
     static constexpr int SMEM_TILES = 1 + NS;
-    static constexpr int XCH_BYTES = (2 * KSPLIT + KSPLIT) * BM * 4; // row-max exchange (2 parities) + row sums
     static constexpr int BAR_BYTES = 256;
-    static constexpr int SMEM_BYTES = 1024 /*align slack*/ + SMEM_TILES * TILE_BYTES + XCH_BYTES + BAR_BYTES;
+    static constexpr int XCH_BYTES = (2 * KSPLIT + KSPLIT) * BM * 4; // static smem: row-max exchange + row sums
+    static constexpr int SMEM_BYTES = 1024 /*align slack*/ + SMEM_TILES * TILE_BYTES + BAR_BYTES;
     static constexpr uint32_t TMEM_COLS = 512;           // S0 | S1 | O (power of two >= 256 + D)
     // O columns are handled (rescale, store) in 32-column slices, one per softmax warp kq < D/32, so every
     // tcgen05.ld/st of O is a 32-column-aligned x32 access.
@@ -97,7 +97,7 @@ struct Cfg {
 #else
     static constexpr int POLY_FROM = 6;
 #endif
-    static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+    static_assert(SMEM_BYTES + XCH_BYTES <= 227 * 1024, "shared memory");
 };
 
 __device__ __forceinline__ int chunk_off(int c) { return c * (BM * 128); }  // Q/K chunk c byte offset in a tile
@@ -109,6 +109,7 @@ struct SmemBars {
     uint64_t s_full[2];       // [S buffer]
     uint64_t p_full[2][2];    // [S buffer][key half]
     uint64_t o_done;          // one phase per completed PV(j)
+    uint64_t o_final;         // all PVs completed (epilogue)
     uint32_t tmem_base;
 };
 
@@ -144,9 +145,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sQ = smem;                                        // 1 tile
     uint8_t *sKV = smem + C::TILE_BYTES;                       // NS tiles
-    float *xmax = reinterpret_cast<float *>(smem + C::SMEM_TILES * C::TILE_BYTES);  // [parity][KSPLIT][row]
-    float *xsum = xmax + 2 * KSPLIT * BM;                                           // [KSPLIT][row]
-    SmemBars *bars = reinterpret_cast<SmemBars *>(smem + C::SMEM_TILES * C::TILE_BYTES + C::XCH_BYTES);
+    // row-max / row-sum exchange between the KSPLIT warps of a row quarter: a static __shared__ array, so
+    // the compiler emits STS/LDS (a pointer derived from the aligned dynamic base would be generic LD/ST)
+    __shared__ float xmax[2 * KSPLIT * BM];   // [iteration parity][key slice][row]
+    __shared__ float xsum[KSPLIT * BM];       // [key slice][row]
+    SmemBars *bars = reinterpret_cast<SmemBars *>(smem + C::SMEM_TILES * C::TILE_BYTES);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -169,6 +172,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_init(&bars->p_full[s][1], NUM_SOFTMAX_WARPS / 2);
         }
         ptx::mbar_init(&bars->o_done, 1);
+        ptx::mbar_init(&bars->o_final, 1);
         ptx::fence_mbar_init();
     }
     if (warp == PRODUCER_WARP && lane == 0) {
@@ -316,6 +320,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                     if (hf == 1) {
                         ptx::mma_commit(&bars->o_done);
+                        if (j == n_kv - 1) ptx::mma_commit(&bars->o_final);
                         ptx::mma_commit_mc(&bars->kv_empty[slotV], 0x3);
                     }
                 }
@@ -412,7 +417,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 // O *= factor for the moved rows (others by exactly 1) after PV(j-1) completed and before
                 // PV(j) of either key half (the half-0 PV also updates this warp's O slice).
                 if (j > 0 && kq < C::NSLICE) {
-                    ptx::mbar_wait(&bars->o_done, (j - 1) & 1);
+                    // unambiguous: S(j) completed, so PV(j-2) did (issued before QK(j)); o_done is <= 1 phase behind
+                ptx::mbar_wait(&bars->o_done, (j - 1) & 1);
                     ptx::tc_fence_after();
                     uint32_t r[C::DW];
                     ptx::tmem_ld_cols<C::DW>(tO, r);
@@ -444,7 +450,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int k = 0; k < KSPLIT; ++k) lsum += xsum[k * BM + row];
         const float inv_l = 1.f / lsum;
-        ptx::mbar_wait(&bars->o_done, (n_kv - 1) & 1);
+        ptx::mbar_wait(&bars->o_final, 0);   // (o_done could be two phases behind here)
         ptx::tc_fence_after();
         const long long srow = (long long)qtile * BM + row;
         const bool valid = srow < args.Sq;      // tcgen05.ld is warp-collective: every lane loads, valid lanes store
