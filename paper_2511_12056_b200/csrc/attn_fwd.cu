@@ -5,25 +5,29 @@
 // which is Alg. 1 line 3 `attention(Q[:,j],K[:,j],V[:,j])` for a
 // group of heads; the scale 1/sqrt(D) is the north star's (R1).
 //
-// Design (DESIGN.md §Kernels / attention), one CTA = one 128-row query tile of one (b, head); clusters of
-// two CTAs (adjacent query tiles of the same head) share every K/V tile through TMA multicast:
-//   warps 0..15  softmax / correction / epilogue: warp w owns TMEM lanes 32*(w%4)..+31 (its rows, = its SM
-//                sub-partition) and keys [32*(w/4), 32*(w/4)+32) of every 128-key tile; the 4 warps of a row
-//                quarter assemble the row max through shared memory (named barrier) every tile.
-//   warp 16      TMA producer: Q once, then K/V tiles through an NS-slot shared-memory ring in the order the
-//                MMA consumes them (K0, K1, V0, K2, V1, K3, ...); each CTA fetches 64 of the 128 rows of every
-//                tile and multicasts them to both CTAs of the pair.
-//   warp 17      TMEM allocator + tcgen05.mma issuer (one elected lane; highest warp id = scheduling priority).
-//   TMEM: S double buffer at columns [0,128) and [128,256) (fp32), O at [256, 256+D).
-//   * S(j) = Q K_j^T   tcgen05.mma SS, M=128 N=128 into S buffer j%2, so QK^T of tile j+1 runs while the
-//     softmax of tile j is in progress.
-//   * P(j) (bf16) is written by each softmax warp over the first 16 columns of its own 32 score columns (scores
-//     it has already read); key half 0 (keys 0..63) and half 1 are released to the MMA issuer separately.
-//   * O += P(j) V_j     tcgen05.mma TS (A = P from TMEM, B = V MN-major, N = D in one instruction).
-//   * online softmax in fp32, base 2 with log2(e)/sqrt(D) folded into one FFMA2; the running max only moves
-//     when it grows by more than 2^8 (conditional rescale; exact, since the final 1/l uses the same max).  The
-//     decision is per row, so a row's result does not depend on the other rows of its tile (bit-identical
-//     across stage splits).  A quarter of the exponentials run as a degree-3 polynomial on the FMA pipe.
+// Design, one CTA = one 128-row query tile of one (b, head); clusters of two CTAs
+// (adjacent query tiles of the same head) share every K/V tile through TMA multicast.
+//   * The KV tiles of a row are split by parity: warps 0..3 ("even" softmax warps, one per TMEM lane
+//     quarter = SM sub-partition) process tiles 0, 2, 4, ..., warps 4..7 ("odd") tiles 1, 3, 5, ...
+//     Each parity keeps its own running max / sum and its own O accumulator in TMEM, so the two warps
+//     of a sub-partition never wait for each other inside the loop (they work on different tiles
+//     concurrently, hiding each other's latencies); the two partial softmaxes are merged once in the
+//     epilogue:  O = (O_e 2^(m_e-m) + O_o 2^(m_o-m)) / (l_e 2^(m_e-m) + l_o 2^(m_o-m)),  m = max(m_e, m_o).
+//   * TMEM: S buffers for even / odd tiles at columns [0,128) / [128,256) (fp32), O_even at [256, 256+D),
+//     O_odd at [384, 384+D).
+//   warp 8  TMA producer: Q once, then K/V tiles through an NS-slot smem ring in consumption order
+//           (K0, K1, V0, K2, V1, K3, ...); each CTA of the pair fetches 64 of the 128 rows of every tile
+//           and multicasts them to both CTAs.
+//   warp 9  TMEM allocator + tcgen05.mma issuer (one elected lane; highest warp id = scheduler priority):
+//           S(j) = Q K_j^T (SS, M=N=128) into S buffer j%2; O_{j%2} += P(j) V_j (TS: P from TMEM, V MN-major,
+//           N = D in one instruction), released in two key halves; S(j+2) is issued right after PV(j).
+//   * softmax (one thread per row, 128 keys): two-pass over TMEM (row max, then exp2 in two 64-key halves,
+//     each released to the MMA issuer as soon as its bf16 P is in TMEM, written over scores already read);
+//     fp32, base 2 with log2(e)/sqrt(D) folded into one FFMA2; the running max only moves when it grows
+//     by more than 2^8 (conditional rescale of that parity's O; exact, the final 1/l uses the same max);
+//     a quarter of the exponentials run as a degree-3 polynomial on the FMA pipe.  Every decision is per
+//     row and the even/odd split depends only on the KV tile index, so a row's result does not depend on
+//     which other rows share its tile (bit-identical across stage splits).
 //   * keys >= Skv (ragged tail, TMA zero-filled) get score -inf; query rows >= Sq are not stored.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -41,17 +45,13 @@ namespace {
 
 constexpr int BM = 128;        // query rows per CTA (MMA M)
 constexpr int BN = 128;        // keys per tile (MMA N of QK^T, K of PV)
-// Softmax warps per row quarter: each owns BN/KSPLIT keys of every KV tile for 32 rows.  Four warps
-// per SM sub-partition hide the fixed-latency dependency stalls of the exp/sum/pack chain.
-constexpr int KSPLIT = 4;
-constexpr int KPW = BN / KSPLIT;                 // keys per softmax warp (32)
-constexpr int NUM_SOFTMAX_WARPS = 4 * KSPLIT;
-constexpr int NUM_WARPS = NUM_SOFTMAX_WARPS + 2;
-constexpr int NUM_THREADS = NUM_WARPS * 32;
-constexpr int PRODUCER_WARP = NUM_SOFTMAX_WARPS;
+constexpr int NUM_SOFTMAX_WARPS = 8;   // 4 lane quarters x 2 tile parities
+constexpr int PRODUCER_WARP = 8;
 // The MMA issuer has the highest warp id: the warp scheduler favours higher ids, and its few instructions
 // must not queue behind the softmax warps that share its SM sub-partition.
-constexpr int MMA_WARP = NUM_SOFTMAX_WARPS + 1;
+constexpr int MMA_WARP = 9;
+constexpr int NUM_WARPS = 10;
+constexpr int NUM_THREADS = NUM_WARPS * 32;
 constexpr float RESCALE_TAU = 8.0f;  // log2 domain: raise the running max only if it grows by > 2^8
 
 #ifdef SPA_ATTN_TRACE
@@ -80,18 +80,14 @@ struct Cfg {
     static constexpr int V_ATOMS = D / V_ATOM_COLS;
     static constexpr int V_ATOM_BYTES = BM * V_ATOM_COLS * 2;
     static constexpr int TILE_BYTES = BM * D * 2;
-    static constexpr int NS = (D == 128) ? 5 : 8;         // K/V ring slots
+    static constexpr int NS = (D == 128) ? 5 : (D == 96 ? 7 : 8);   // K/V ring slots
     static constexpr int SMEM_TILES = 1 + NS;
-    static constexpr int BAR_BYTES = 256;
-    static constexpr int XCH_BYTES = (2 * KSPLIT + KSPLIT) * BM * 4; // static smem: row-max exchange + row sums
+    static constexpr int BAR_BYTES = 512;
+    static constexpr int XCH_BYTES = 4 * BM * 4;         // static smem: per-row (m, l) of both parities
     static constexpr int SMEM_BYTES = 1024 /*align slack*/ + SMEM_TILES * TILE_BYTES + BAR_BYTES;
-    static constexpr uint32_t TMEM_COLS = 512;           // S0 | S1 | O (power of two >= 256 + D)
-    // O columns are handled (rescale, store) in 32-column slices, one per softmax warp kq < D/32, so every
-    // tcgen05.ld/st of O is a 32-column-aligned x32 access.
-    static constexpr int DW = 32;
-    static constexpr int NSLICE = D / 32;
+    static constexpr uint32_t TMEM_COLS = 512;           // S_even | S_odd | O_even | O_odd
+    static constexpr int DH = D / 2;                     // O columns each parity warp merges and stores
     // exp2 split: key pairs with (i & 7) >= POLY_FROM use the FMA-pipe polynomial, the rest MUFU.EX2.
-    // 6 = 1/4 polynomial was fastest at D = 64, 96 and 128 (sweep of 2/4/6/8 on B200).
 #ifdef SPA_POLY_FROM
     static constexpr int POLY_FROM = SPA_POLY_FROM;
 #else
@@ -106,23 +102,20 @@ struct SmemBars {
     uint64_t q_full;
     uint64_t kv_full[8];
     uint64_t kv_empty[8];
-    uint64_t s_full[2];       // [S buffer]
-    uint64_t p_full[2][2];    // [S buffer][key half]
-    uint64_t o_done;          // one phase per completed PV(j)
+    uint64_t s_full[2];       // [tile parity]: S(j) complete
+    uint64_t p_full[2][2];    // [tile parity][key half]: P(j) half written by the 4 warps of that parity
     uint64_t o_final;         // all PVs completed (epilogue)
     uint32_t tmem_base;
 };
+static_assert(sizeof(SmemBars) <= 512, "barrier block");
 
-// 2^x on the FMA pipe: x = n + f (n = round(x), |f| <= 1/2), 2^f by a degree-3 fit (max rel err 7.5e-5,
-// far below the bf16 rounding of P), 2^n by adding n to the exponent field.  x is clamped at -125 so the
-// result stays a normal number (p >= 0.7 has exponent >= 126).
-
-// Two ex2_poly at once in f32x2 arithmetic (same operations per element, so identical results).
+// Two exp2 at once in f32x2 arithmetic: x = n + f (n = round(x), |f| <= 1/2), 2^f by a degree-3 fit (max rel
+// err 7.5e-5, far below the bf16 rounding of P), 2^n added to the exponent field; x >= -125 keeps it normal.
 __device__ __forceinline__ void ex2_poly2(uint64_t X, float &y0, float &y1) {
     float x0, x1;
     ptx::f2unpack(X, x0, x1);
     const uint64_t Xc = ptx::f2pack(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
-    const uint64_t T = ptx::fadd2(Xc, ptx::f2pack(12582912.f, 12582912.f));
+    const uint64_t T = ptx::fadd2(Xc, ptx::f2pack(12582912.f, 12582912.f));   // 1.5*2^23: low bits = round(x)
     const uint64_t F = ptx::fsub2(Xc, ptx::fadd2(T, ptx::f2pack(-12582912.f, -12582912.f)));
     uint64_t P = ptx::ffma2(ptx::f2pack(0.0551716611f, 0.0551716611f), F, ptx::f2pack(0.242611152f, 0.242611152f));
     P = ptx::ffma2(P, F, ptx::f2pack(0.693260968f, 0.693260968f));
@@ -145,11 +138,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sQ = smem;                                        // 1 tile
     uint8_t *sKV = smem + C::TILE_BYTES;                       // NS tiles
-    // row-max / row-sum exchange between the KSPLIT warps of a row quarter: a static __shared__ array, so
-    // the compiler emits STS/LDS (a pointer derived from the aligned dynamic base would be generic LD/ST)
-    __shared__ float xmax[2 * KSPLIT * BM];   // [iteration parity][key slice][row]
-    __shared__ float xsum[KSPLIT * BM];       // [key slice][row]
     SmemBars *bars = reinterpret_cast<SmemBars *>(smem + C::SMEM_TILES * C::TILE_BYTES);
+    __shared__ float xml[4 * BM];   // [parity][row]: m, then [2 + parity][row]: l (epilogue merge)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -164,20 +154,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_init(&bars->kv_full[i], 1);
             ptx::mbar_init(&bars->kv_empty[i], 2);   // released by the MMA issuers of both CTAs of the pair
         }
-        for (int s = 0; s < 2; ++s) {
-            ptx::mbar_init(&bars->s_full[s], 1);
-            // half 0: P written by the warps of keys 0..63 + "O corrected" from the warps of keys 64..127
-            // (PV of half 0 updates all of O's columns, so every O slice must be rescaled first)
-            ptx::mbar_init(&bars->p_full[s][0], NUM_SOFTMAX_WARPS);
-            ptx::mbar_init(&bars->p_full[s][1], NUM_SOFTMAX_WARPS / 2);
+        for (int t = 0; t < 2; ++t) {
+            ptx::mbar_init(&bars->s_full[t], 1);
+            ptx::mbar_init(&bars->p_full[t][0], 4);   // one arrival per softmax warp of that parity
+            ptx::mbar_init(&bars->p_full[t][1], 4);
         }
-        ptx::mbar_init(&bars->o_done, 1);
         ptx::mbar_init(&bars->o_final, 1);
         ptx::fence_mbar_init();
     }
     if (warp == PRODUCER_WARP && lane == 0) {
         ptx::prefetch_tmap(&tmQa); ptx::prefetch_tmap(&tmKa); ptx::prefetch_tmap(&tmVa);
-        if (C::N64) { ptx::prefetch_tmap(&tmQb); ptx::prefetch_tmap(&tmKb); ptx::prefetch_tmap(&tmVb); }
+        if (C::N64) { ptx::prefetch_tmap(&tmQb); ptx::prefetch_tmap(&tmKb); }
     }
     if (warp == MMA_WARP) {
         ptx::tmem_alloc(&bars->tmem_base, C::TMEM_COLS);
@@ -194,35 +181,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // ------------------------------------------------------------ TMA producer
         const uint64_t pol_q = ptx::policy_evict_first();
         const uint64_t pol_kv = ptx::policy_evict_last();
-        // Q/K style (K-major) tile: chunk 0 = cols 0..63 (SW128); chunk 1 = cols 64.. (SW128 or SW64)
-        auto load_qk = [&](const CUtensorMap *m64, const CUtensorMap *m32, uint64_t *bar, uint8_t *dst, int row,
-                           uint64_t pol) {
-            ptx::tma_load_4d(m64, bar, dst, 0, head, row, b, pol);
-            if (C::N128 == 2) ptx::tma_load_4d(m64, bar, dst + chunk_off(1), 64, head, row, b, pol);
-            if (C::N64) ptx::tma_load_4d(m32, bar, dst + chunk_off(1), 64, head, row, b, pol);
-        };
         if (lane == 0) {
             ptx::mbar_arrive_expect_tx(&bars->q_full, C::TILE_BYTES);
-            load_qk(&tmQa, &tmQb, &bars->q_full, sQ, qtile * BM, pol_q);
+            ptx::tma_load_4d(&tmQa, &bars->q_full, sQ, 0, head, qtile * BM, b, pol_q);
+            if (C::N128 == 2) ptx::tma_load_4d(&tmQa, &bars->q_full, sQ + chunk_off(1), 64, head, qtile * BM, b, pol_q);
+            if (C::N64) ptx::tma_load_4d(&tmQb, &bars->q_full, sQ + chunk_off(1), 64, head, qtile * BM, b, pol_q);
         }
         int cnt = 0;
         // Each CTA of the pair fetches rows [64*crank, 64*crank+64) of every K/V tile and multicasts them to
-        // both CTAs (same smem offset); each CTA's kv_full expects the whole tile.  Halves the L2->SMEM
-        // traffic per query row relative to unshared 128-row tiles.
+        // both CTAs (same smem offset); each CTA's kv_full expects the whole tile.
         auto load = [&](bool isV, int j) {
             const int slot = cnt % C::NS;
             ptx::mbar_wait(&bars->kv_empty[slot], ((cnt / C::NS) & 1) ^ 1);
-            if (lane == 0) TRACE(j, isV ? 7 : 2);
             if (lane == 0) {
                 uint8_t *dst = sKV + slot * C::TILE_BYTES;
                 uint64_t *bar = &bars->kv_full[slot];
                 ptx::mbar_arrive_expect_tx(bar, C::TILE_BYTES);
                 const int row = j * BN + (int)crank * (BN / 2);
                 if (isV) {
-                    const CUtensorMap *mv = &tmVa;
 #pragma unroll
                     for (int a = 0; a < C::V_ATOMS; ++a)
-                        ptx::tma_load_4d_mc(mv, bar, dst + a * C::V_ATOM_BYTES + crank * (C::V_ATOM_BYTES / 2),
+                        ptx::tma_load_4d_mc(&tmVa, bar, dst + a * C::V_ATOM_BYTES + crank * (C::V_ATOM_BYTES / 2),
                                             a * C::V_ATOM_COLS, head, row, b, 0x3, pol_kv);
                 } else {
                     ptx::tma_load_4d_mc(&tmKa, bar, dst + crank * (BM / 2) * 128, 0, head, row, b, 0x3, pol_kv);
@@ -250,7 +229,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         constexpr uint32_t IDESC_PV = ptx::idesc_bf16(BM, D, 0, 1);
         const uint32_t qa = ptx::smem_u32(sQ);
         const uint32_t sKV_addr = ptx::smem_u32(sKV);
-        const uint32_t tO = tmem + 256;
 
         int cnt = 0;
         auto acquire = [&]() -> int {   // next ring slot, waiting for its data
@@ -269,10 +247,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool leader = ptx::elect_one();
         // S(j) = Q K_j^T into S buffer j%2: K-major A (Q) and B (K), 16-element k-steps per swizzle chunk.
         auto issue_qk = [&](int j) {
-            if (leader) TRACE(j, 12);
             const int slot = acquire();
             if (leader) {
-                TRACE(j, 13);
                 const uint64_t so = (uint64_t)(slot * C::TILE_BYTES) >> 4;
                 const uint32_t d = tmem + (j & 1) * 128;
 #pragma unroll
@@ -282,9 +258,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                     for (int kk = 0; kk < ksteps; ++kk) {
                         const uint64_t off = (uint64_t)((sw64 ? 0 : c * (BM * 128)) + kk * 32) >> 4;
-                        const uint64_t ad = (sw64 ? dQ64 : dQ128) + off;
-                        const uint64_t bd = (sw64 ? dK64 : dK128) + so + off;
-                        ptx::mma_ss(d, ad, bd, IDESC_QK, (c | kk) ? 1u : 0u);
+                        ptx::mma_ss(d, (sw64 ? dQ64 : dQ128) + off, (sw64 ? dK64 : dK128) + so + off, IDESC_QK,
+                                    (c | kk) ? 1u : 0u);
                     }
                 }
                 ptx::mma_commit(&bars->s_full[j & 1]);
@@ -297,31 +272,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         issue_qk(0);
         if (n_kv > 1) issue_qk(1);
         for (int j = 0; j < n_kv; ++j) {
-            const int buf = j & 1;
-            const uint32_t tS = tmem + buf * 128;
-            if (leader) TRACE(j, 14);
+            const int t = j & 1;
+            const uint32_t tS = tmem + t * 128;
+            const uint32_t tO = tmem + 256 + t * 128;
             const int slotV = acquire();
-            if (leader) TRACE(j, 15);
             const uint64_t dVs = dV + ((uint64_t)(slotV * C::TILE_BYTES) >> 4);
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
-                ptx::mbar_wait(&bars->p_full[buf][hf], (j >> 1) & 1);
+                ptx::mbar_wait(&bars->p_full[t][hf], (j >> 1) & 1);
                 ptx::tc_fence_after();
                 if (leader) {
                     TRACE(j, hf);
-                    // O (+)= P(j)[keys 64hf..64hf+63] V_j[those keys]; the P of keys [KPW*k, KPW*k+KPW) sits in
-                    // columns [KPW*k, KPW*k + KPW/2) (written over scores its warp had already read)
+                    // O_t (+)= P(j)[keys 64hf..64hf+63] V_j[those keys]; that P half sits in columns 64hf..64hf+31
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const int key16 = hf * 4 + kk;
-                        const int pcol = (key16 * 16 / KPW) * KPW + (key16 * 16 % KPW) / 2;
-                        ptx::mma_ts(tO, tS + pcol, dVs + ((uint64_t)(key16 * 16 * rowb) >> 4), IDESC_PV,
-                                    (j > 0 || key16 > 0) ? 1u : 0u);
+                        ptx::mma_ts(tO, tS + hf * 64 + kk * 8, dVs + ((uint64_t)(key16 * 16 * rowb) >> 4), IDESC_PV,
+                                    (j >= 2 || key16 > 0) ? 1u : 0u);
                     }
                     if (hf == 1) {
-                        ptx::mma_commit(&bars->o_done);
-                        if (j == n_kv - 1) ptx::mma_commit(&bars->o_final);
                         ptx::mma_commit_mc(&bars->kv_empty[slotV], 0x3);
+                        if (j == n_kv - 1) ptx::mma_commit(&bars->o_final);
                     }
                 }
                 __syncwarp();
@@ -330,49 +301,99 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else {
         // ------------------------------------------------------------ softmax / correction / epilogue
-        const int kq = warp >> 2;                      // key slice [KPW*kq, KPW*kq + KPW) of every KV tile
+        const int t = warp >> 2;                       // tile parity handled by this warp
         const int wq = warp & 3;                       // TMEM lane quarter this warp may access (= SMSP)
         const int row = wq * 32 + lane;                // row within the tile
-        const int hf = kq / (KSPLIT / 2);              // which P half (keys 0..63 / 64..127) this warp feeds
-        const uint32_t bar_id = 1 + wq;                // named barrier of the KSPLIT warps sharing these rows
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-        const uint32_t tO = tmem + lane_base + 256 + kq * C::DW;   // this warp's slice of O's columns
+        const uint32_t tS = tmem + lane_base + t * 128;
+        const uint32_t tO = tmem + lane_base + 256 + t * 128;
         const float sl2 = args.scale_log2;
+        const uint64_t SL2 = ptx::f2pack(sl2, sl2);
         const int last_valid = args.Skv - (n_kv - 1) * BN;   // valid keys in the last tile (1..128)
-        const int key0 = kq * KPW;
-        const bool tr = (lane == 0 && wq == 0 && (kq % (KSPLIT / 2)) == 0);
+        const bool tr = (lane == 0 && wq == 0);
 
-        float m = -INFINITY;   // running max, already scaled to the log2 domain (same in all KSPLIT warps)
-        float l = 0.f;         // this warp's running sum of p (fp32)
-        for (int j = 0; j < n_kv; ++j) {
-            const int buf = j & 1;
-            const uint32_t tS = tmem + lane_base + buf * 128 + key0;   // this warp's KPW scores
+        float m = -INFINITY;   // running max of this parity's tiles, scaled to the log2 domain
+        float l = 0.f;         // running sum of p of this parity's tiles (fp32)
+        for (int j = t; j < n_kv; j += 2) {
             const bool masked = (j == n_kv - 1) && (last_valid < BN);
-            if (tr) TRACE(j, 3 + 5 * hf);
-            ptx::mbar_wait(&bars->s_full[buf], (j >> 1) & 1);
+            if (tr) TRACE(j, 3 + 5 * t);
+            ptx::mbar_wait(&bars->s_full[t], (j >> 1) & 1);
             ptx::tc_fence_after();
-            if (tr) TRACE(j, 4 + 5 * hf);
-            // One TMEM read of this warp's KPW scores: slice max -> row max assembled from the KSPLIT slices
-            // through shared memory -> conditional rescale -> P.
-            uint32_t sv[KPW];
-            ptx::tmem_ld_cols<KPW>(tS, sv);
-            ptx::tmem_wait_ld();
-            if (masked) {
+            if (tr) TRACE(j, 4 + 5 * t);
+            // pass 1: row max over the 128 keys, two rounds of 64 columns (keeps registers low)
+            float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
 #pragma unroll
-                for (int i = 0; i < KPW; ++i)
-                    if (key0 + i >= last_valid) sv[i] = __float_as_uint(-INFINITY);
+            for (int h = 0; h < 2; ++h) {
+                uint32_t sa[32], sb[32];
+                ptx::tmem_ld32(tS + 64 * h, sa);
+                ptx::tmem_ld32(tS + 64 * h + 32, sb);
+                ptx::tmem_wait_ld();
+                if (masked) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        if (64 * h + i >= last_valid) sa[i] = 0xff800000u;
+                        if (64 * h + 32 + i >= last_valid) sb[i] = 0xff800000u;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    m0 = fmaxf(m0, __uint_as_float(sa[i]));
+                    m1 = fmaxf(m1, __uint_as_float(sa[i + 1]));
+                    m2 = fmaxf(m2, __uint_as_float(sb[i]));
+                    m3 = fmaxf(m3, __uint_as_float(sb[i + 1]));
+                }
             }
-            uint32_t pk[KPW / 2];
-            float lsum;
-            auto exps = [&](float mcur) {
-                const uint64_t SL2 = ptx::f2pack(sl2, sl2), NEGM = ptx::f2pack(-mcur, -mcur);
-                uint64_t L0 = ptx::f2pack(0.f, 0.f), L1 = L0;
+            const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl2;
+            if (tr) TRACE(j, 5 + 5 * t);
+            const bool resc = mx > m + RESCALE_TAU;   // also true on this parity's first tile (m = -inf)
+            if (__any_sync(0xffffffffu, resc)) {
+                float factor = 1.f;
+                if (resc) {
+                    factor = ptx::ex2(m - mx);        // 0 on the first tile
+                    m = mx;
+                }
+                l *= factor;
+                // O_t *= factor for the moved rows (others by exactly 1).  PV(j-2), the last product into
+                // O_t, completed before S(j) did (it was issued first), and PV(j) waits for this P.
+                if (j >= 2) {
 #pragma unroll
-                for (int i = 0; i < KPW / 2; ++i) {
-                    const uint64_t X = ptx::ffma2(ptx::f2pack(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])),
-                                                  SL2, NEGM);
+                    for (int c = 0; c < D / 32; ++c) {
+                        uint32_t r[32];
+                        ptx::tmem_ld32(tO + 32 * c, r);
+                        ptx::tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * factor);
+                        ptx::tmem_st32(tO + 32 * c, r);
+                    }
+                }
+            }
+            // pass 2, per 64-key half: reload the scores, P = exp2(s*sl2 - m) in f32x2 pairs (MUFU or FMA-pipe
+            // polynomial by column), bf16 pairs written over the half's first 32 score columns (already read),
+            // released to the MMA issuer.
+            const uint64_t NEGM = ptx::f2pack(-m, -m);
+            uint64_t L0 = ptx::f2pack(0.f, 0.f), L1 = L0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint32_t sa[32], sb[32];
+                ptx::tmem_ld32(tS + 64 * h, sa);
+                ptx::tmem_ld32(tS + 64 * h + 32, sb);
+                ptx::tmem_wait_ld();
+                if (masked) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        if (64 * h + i >= last_valid) sa[i] = 0xff800000u;
+                        if (64 * h + 32 + i >= last_valid) sb[i] = 0xff800000u;
+                    }
+                }
+                uint32_t pk[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int e = 2 * i;
+                    const uint32_t u0 = e < 32 ? sa[e] : sb[e - 32];
+                    const uint32_t u1 = e + 1 < 32 ? sa[e + 1] : sb[e + 1 - 32];
+                    const uint64_t X = ptx::ffma2(ptx::f2pack(__uint_as_float(u0), __uint_as_float(u1)), SL2, NEGM);
                     float p0, p1;
-                    if (((2 * i) & 7) >= C::POLY_FROM) {
+                    if ((e & 7) >= C::POLY_FROM) {
                         ex2_poly2(X, p0, p1);
                     } else {
                         float x0, x1;
@@ -384,92 +405,58 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     else L0 = ptx::fadd2(L0, ptx::f2pack(p0, p1));
                     pk[i] = ptx::pack_bf16x2(p0, p1);
                 }
+                ptx::tmem_st32(tS + 64 * h, pk);
+                ptx::tmem_wait_st();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&bars->p_full[t][h]);
+            }
+            {
                 float a0, a1, b0, b1;
                 ptx::f2unpack(L0, a0, a1);
                 ptx::f2unpack(L1, b0, b1);
-                lsum = (a0 + b0) + (a1 + b1);
-            };
-            float mx;
-            {
-                float m0 = __uint_as_float(sv[0]), m1 = __uint_as_float(sv[1]);
-#pragma unroll
-                for (int i = 2; i < KPW; i += 2) {
-                    m0 = fmaxf(m0, __uint_as_float(sv[i]));
-                    m1 = fmaxf(m1, __uint_as_float(sv[i + 1]));
-                }
-                mx = fmaxf(m0, m1);
+                l += (a0 + b0) + (a1 + b1);
             }
-            float *xm = xmax + (j & 1) * KSPLIT * BM;
-            xm[kq * BM + row] = mx;
-            ptx::named_bar_sync(bar_id, 32 * KSPLIT);
-#pragma unroll
-            for (int k = 0; k < KSPLIT; ++k) mx = fmaxf(mx, xm[k * BM + row]);
-            mx *= sl2;
-            if (tr) TRACE(j, 5 + 5 * hf);
-            const bool resc = mx > m + RESCALE_TAU;      // also true on the first tile (m = -inf)
-            if (__any_sync(0xffffffffu, resc)) {
-                float factor = 1.f;
-                if (resc) {
-                    factor = ptx::ex2(m - mx);            // 0 on the first tile
-                    m = mx;
-                }
-                l *= factor;
-                // O *= factor for the moved rows (others by exactly 1) after PV(j-1) completed and before
-                // PV(j) of either key half (the half-0 PV also updates this warp's O slice).
-                if (j > 0 && kq < C::NSLICE) {
-                    // unambiguous: S(j) completed, so PV(j-2) did (issued before QK(j)); o_done is <= 1 phase behind
-                ptx::mbar_wait(&bars->o_done, (j - 1) & 1);
-                    ptx::tc_fence_after();
-                    uint32_t r[C::DW];
-                    ptx::tmem_ld_cols<C::DW>(tO, r);
-                    ptx::tmem_wait_ld();
-#pragma unroll
-                    for (int i = 0; i < C::DW; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * factor);
-                    ptx::tmem_st_cols<C::DW>(tO, r);
-                    ptx::tmem_wait_st();
-                }
-            }
-            exps(m);
-            l += lsum;
-            if (hf == 1) {   // this warp's O slice is ready for PV(j) of key half 0
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&bars->p_full[buf][0]);
-            }
-            ptx::tmem_st_cols<KPW / 2>(tS, pk);   // over scores this warp has already consumed
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&bars->p_full[buf][hf]);
-            if (tr) TRACE(j, 6 + 5 * hf);
+            if (tr) TRACE(j, 6 + 5 * t);
         }
-        // ------------------------------------------------------------ epilogue: O / l -> bf16 -> global
-        xsum[kq * BM + row] = l;
-        ptx::named_bar_sync(bar_id, 32 * KSPLIT);
-        float lsum = 0.f;
-#pragma unroll
-        for (int k = 0; k < KSPLIT; ++k) lsum += xsum[k * BM + row];
-        const float inv_l = 1.f / lsum;
-        ptx::mbar_wait(&bars->o_final, 0);   // (o_done could be two phases behind here)
+        // ------------------------------------------------------------ epilogue: merge parities, O / l -> global
+        xml[t * BM + row] = m;
+        xml[(2 + t) * BM + row] = l;
+        ptx::named_bar_sync(1 + wq, 64);               // the two parity warps of this lane quarter
+        const float me = xml[row], mo = xml[BM + row];
+        const float mm = fmaxf(me, mo);
+        const float se = (me == -INFINITY) ? 0.f : ptx::ex2(me - mm);   // odd parity may have no tile (n_kv = 1)
+        const float so = (mo == -INFINITY) ? 0.f : ptx::ex2(mo - mm);
+        const float inv = 1.f / (xml[2 * BM + row] * se + xml[3 * BM + row] * so);
+        const float ce = se * inv, co = so * inv;
+        ptx::mbar_wait(&bars->o_final, 0);
         ptx::tc_fence_after();
         const long long srow = (long long)qtile * BM + row;
         const bool valid = srow < args.Sq;      // tcgen05.ld is warp-collective: every lane loads, valid lanes store
-        if (kq < C::NSLICE) {   // warps kq >= D/32 own no O slice (D = 64 / 96)
-            uint32_t r[C::DW];
-            ptx::tmem_ld_cols<C::DW>(tO, r);
+        uint4 *dst = reinterpret_cast<uint4 *>(args.O + (long long)b * args.o_batch_stride + srow * args.o_tok_stride +
+                                               (long long)head * D);
+        // this warp merges and stores O columns [t*DH, t*DH + DH) in chunks of 16
+        const uint32_t tOe = tmem + lane_base + 256, tOo = tmem + lane_base + 384;
+#pragma unroll
+        for (int c = 0; c < C::DH / 16; ++c) {
+            const int col = t * C::DH + 16 * c;
+            uint32_t re[16], ro[16];
+            ptx::tmem_ld16(tOe + col, re);
+            if (n_kv > 1) ptx::tmem_ld16(tOo + col, ro);   // O_odd is never written when n_kv == 1
             ptx::tmem_wait_ld();
-            if (valid) {
-                uint4 *dst = reinterpret_cast<uint4 *>(args.O + (long long)b * args.o_batch_stride +
-                                                       srow * args.o_tok_stride + (long long)head * D + kq * C::DW);
+            uint32_t w[8];
 #pragma unroll
-                for (int v = 0; v < C::DW / 8; ++v) {
-                    uint32_t w[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        w[u] = ptx::pack_bf16x2(__uint_as_float(r[8 * v + 2 * u]) * inv_l,
-                                                __uint_as_float(r[8 * v + 2 * u + 1]) * inv_l);
-                    dst[v] = make_uint4(w[0], w[1], w[2], w[3]);
+            for (int u = 0; u < 8; ++u) {
+                float v0 = __uint_as_float(re[2 * u]) * ce, v1 = __uint_as_float(re[2 * u + 1]) * ce;
+                if (n_kv > 1) {
+                    v0 = fmaf(__uint_as_float(ro[2 * u]), co, v0);
+                    v1 = fmaf(__uint_as_float(ro[2 * u + 1]), co, v1);
                 }
+                w[u] = ptx::pack_bf16x2(v0, v1);
+            }
+            if (valid) {
+                dst[col / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+                dst[col / 8 + 1] = make_uint4(w[4], w[5], w[6], w[7]);
             }
         }
     }

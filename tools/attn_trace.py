@@ -46,6 +46,9 @@ d = T[mid]
 per = np.diff(d[:, 1]).mean()
 ideal = {128: 1024, 96: 768, 64: 512}[args.D]
 print(f"steady-state period per KV tile: {per:.0f} cycles (MMA-bound ideal {ideal} at D={args.D})")
-for h, base in ((0, 3), (1, 8)):
-    print(f"half{h}: wait S {np.mean(d[:, base+1]-d[:, base]):.0f}  ld+max+xchg {np.mean(d[:, base+2]-d[:, base+1]):.0f}  "
-          f"exp+store {np.mean(d[:, base+3]-d[:, base+2]):.0f}")
+# softmax events of tile j are written by the warps of tile parity j % 2 (base 3 or 8)
+js = np.arange(n // 4, 3 * n // 4)
+ev = np.stack([T[j, 3 + 5 * (j % 2): 7 + 5 * (j % 2)] for j in js])   # [tiles, 4]: loop top, S ready, max, P done
+print(f"per tile (its parity's warps): wait S {np.mean(ev[:, 1] - ev[:, 0]):.0f}  max {np.mean(ev[:, 2] - ev[:, 1]):.0f}  "
+      f"exp+store {np.mean(ev[:, 3] - ev[:, 2]):.0f}  (a parity handles every other tile)")
+print(f"MMA: P(j) ready -> P(j+1) ready {np.mean(np.diff(T[js, 1])):.0f} cycles")
