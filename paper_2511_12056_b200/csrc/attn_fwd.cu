@@ -7,27 +7,31 @@
 //
 // Design, one CTA = one 128-row query tile of one (b, head); clusters of two CTAs
 // (adjacent query tiles of the same head) share every K/V tile through TMA multicast.
-//   * The KV tiles of a row are split by parity: warps 0..3 ("even" softmax warps, one per TMEM lane
-//     quarter = SM sub-partition) process tiles 0, 2, 4, ..., warps 4..7 ("odd") tiles 1, 3, 5, ...
-//     Each parity keeps its own running max / sum and its own O accumulator in TMEM, so the two warps
-//     of a sub-partition never wait for each other inside the loop (they work on different tiles
-//     concurrently, hiding each other's latencies); the two partial softmaxes are merged once in the
-//     epilogue:  O = (O_e 2^(m_e-m) + O_o 2^(m_o-m)) / (l_e 2^(m_e-m) + l_o 2^(m_o-m)),  m = max(m_e, m_o).
-//   * TMEM: S buffers for even / odd tiles at columns [0,128) / [128,256) (fp32), O_even at [256, 256+D),
-//     O_odd at [384, 384+D).
-//   warp 8  TMA producer: Q once, then K/V tiles through an NS-slot smem ring in consumption order
-//           (K0, K1, V0, K2, V1, K3, ...); each CTA of the pair fetches 64 of the 128 rows of every tile
+//   * TMEM: three S buffers (fp32, 128 columns each) at [0,128), [128,256), [256,384) and ONE O
+//     accumulator at [384, 384+D).  KV tile j goes to S buffer j%3 and is handled by softmax group j%3
+//     (groups = warps 4g..4g+3, one warp per TMEM lane quarter = SM sub-partition).  Three S buffers make
+//     three independent S -> softmax -> PV chains, so the tensor pipe always has a QK^T or PV product
+//     queued while a group is in its softmax (each group has three tiles of MMA time for one tile of
+//     softmax; the v3 design with two chains was latency-bound: softmax warps idled a third of the time
+//     on S(j)).
+//   * The running max is one per row, shared by all groups: it travels tile to tile through shared
+//     memory (named barrier arrive/sync between the warps of consecutive groups on the same sub-partition),
+//     so every P is relative to the same reference max as O.  It only moves when a tile's row max exceeds
+//     it by more than 2^8 (conditional rescale); then the group that moved it waits for PV(j-1) and rescales
+//     O in TMEM before releasing P(j).  Each group keeps its own partial row sum l_g relative to the last
+//     max it saw; the epilogue merges them.
+//   warp 12 TMA producer (warps 13, 14 idle): Q once, then K/V tiles through an NS-slot smem ring in consumption order
+//           (K0, K1, K2, V0, K3, V1, K4, ...); each CTA of the pair fetches 64 of the 128 rows of every tile
 //           and multicasts them to both CTAs.
-//   warp 9  TMEM allocator + tcgen05.mma issuer (one elected lane; highest warp id = scheduler priority):
-//           S(j) = Q K_j^T (SS, M=N=128) into S buffer j%2; O_{j%2} += P(j) V_j (TS: P from TMEM, V MN-major,
-//           N = D in one instruction), released in two key halves; S(j+2) is issued right after PV(j).
+//   warp 15 TMEM allocator + tcgen05.mma issuer (one elected lane; highest warp id = scheduler priority):
+//           S(j) = Q K_j^T (SS, M=N=128) into S buffer j%3; O += P(j) V_j (TS: P from TMEM, V MN-major,
+//           N = D in one instruction), released in two key halves; S(j+3) is issued right after PV(j).
 //   * softmax (one thread per row, 128 keys): two-pass over TMEM (row max, then exp2 in two 64-key halves,
 //     each released to the MMA issuer as soon as its bf16 P is in TMEM, written over scores already read);
-//     fp32, base 2 with log2(e)/sqrt(D) folded into one FFMA2; the running max only moves when it grows
-//     by more than 2^8 (conditional rescale of that parity's O; exact, the final 1/l uses the same max);
-//     a quarter of the exponentials run as a degree-3 polynomial on the FMA pipe.  Every decision is per
-//     row and the even/odd split depends only on the KV tile index, so a row's result does not depend on
-//     which other rows share its tile (bit-identical across stage splits).
+//     fp32, base 2 with log2(e)/sqrt(D) folded into one FFMA2; a quarter of the exponentials run as a
+//     degree-3 polynomial on the FMA pipe.  Every decision is per row and the group of a tile depends only
+//     on its index, so a row's result does not depend on which other rows share its tile (bit-identical
+//     across stage splits).
 //   * keys >= Skv (ragged tail, TMA zero-filled) get score -inf; query rows >= Sq are not stored.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -45,14 +49,22 @@ namespace {
 
 constexpr int BM = 128;        // query rows per CTA (MMA M)
 constexpr int BN = 128;        // keys per tile (MMA N of QK^T, K of PV)
-constexpr int NUM_SOFTMAX_WARPS = 8;   // 4 lane quarters x 2 tile parities
-constexpr int PRODUCER_WARP = 8;
+constexpr int NG = 3;          // softmax groups = S buffers in TMEM = independent S->softmax->PV chains
+constexpr int NUM_SOFTMAX_WARPS = 4 * NG;
+// Four warpgroups: three of softmax warps, then {producer, 2 idle, MMA}.  The last warpgroup gives its
+// registers to the softmax warps (setmaxnreg): per SM sub-partition 3 x 152 + 56 = 512 registers per lane.
+constexpr int PRODUCER_WARP = NUM_SOFTMAX_WARPS;
 // The MMA issuer has the highest warp id: the warp scheduler favours higher ids, and its few instructions
 // must not queue behind the softmax warps that share its SM sub-partition.
-constexpr int MMA_WARP = 9;
-constexpr int NUM_WARPS = 10;
+constexpr int MMA_WARP = NUM_SOFTMAX_WARPS + 3;
+constexpr int NUM_WARPS = NUM_SOFTMAX_WARPS + 4;
 constexpr int NUM_THREADS = NUM_WARPS * 32;
+constexpr int SOFTMAX_REGS = 152, AUX_REGS = 56;
 constexpr float RESCALE_TAU = 8.0f;  // log2 domain: raise the running max only if it grows by > 2^8
+// named barriers: 0 = __syncthreads; 1 + 3*wq + g = "running max of the previous tile is in xm[] for the
+// warp of group g on lane quarter wq"; 1 + 3*4 = all softmax warps (epilogue merge).
+constexpr uint32_t BAR_EPI = 1 + 3 * 4;
+static_assert(NG == 3, "barrier numbering assumes three groups");
 
 #ifdef SPA_ATTN_TRACE
 // Debug timeline of CTA (0,0,0): g_trace[j][e] = clock64 at event e of KV iteration j (tools/attn_trace.py).
@@ -83,10 +95,12 @@ struct Cfg {
     static constexpr int NS = (D == 128) ? 5 : (D == 96 ? 7 : 8);   // K/V ring slots
     static constexpr int SMEM_TILES = 1 + NS;
     static constexpr int BAR_BYTES = 512;
-    static constexpr int XCH_BYTES = 4 * BM * 4;         // static smem: per-row (m, l) of both parities
+    static constexpr int XCH_BYTES = (1 + 2 * NG) * BM * 4;   // static smem: running max + per-group (m, l)
     static constexpr int SMEM_BYTES = 1024 /*align slack*/ + SMEM_TILES * TILE_BYTES + BAR_BYTES;
-    static constexpr uint32_t TMEM_COLS = 512;           // S_even | S_odd | O_even | O_odd
-    static constexpr int DH = D / 2;                     // O columns each parity warp merges and stores
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr uint32_t O_COL = 128 * NG;          // O accumulator columns [O_COL, O_COL + D)
+    static_assert(O_COL + D <= TMEM_COLS, "TMEM budget");
+    static constexpr int OCHUNKS = D / 16;               // epilogue: 16-column chunks, chunk c by group c % NG
     // exp2 split: key pairs with (i & 7) >= POLY_FROM use the FMA-pipe polynomial, the rest MUFU.EX2.
 #ifdef SPA_POLY_FROM
     static constexpr int POLY_FROM = SPA_POLY_FROM;
@@ -102,9 +116,10 @@ struct SmemBars {
     uint64_t q_full;
     uint64_t kv_full[8];
     uint64_t kv_empty[8];
-    uint64_t s_full[2];       // [tile parity]: S(j) complete
-    uint64_t p_full[2][2];    // [tile parity][key half]: P(j) half written by the 4 warps of that parity
-    uint64_t o_final;         // all PVs completed (epilogue)
+    uint64_t s_full[NG];       // [buffer]: S(j) complete
+    uint64_t p_full[NG][2];    // [buffer][key half]: P(j) half written by the 4 warps of that group
+    uint64_t pv_done[NG];      // [buffer]: PV(j) complete (O may be rescaled)
+    uint64_t o_final;          // all PVs completed (epilogue)
     uint32_t tmem_base;
 };
 static_assert(sizeof(SmemBars) <= 512, "barrier block");
@@ -123,8 +138,9 @@ __device__ __forceinline__ void ex2_poly2(uint64_t X, float &y0, float &y1) {
     float p0, p1, t0, t1;
     ptx::f2unpack(P, p0, p1);
     ptx::f2unpack(T, t0, t1);
-    y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
-    y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+    // bits(T) = bits(1.5*2^23) + n and bits(1.5*2^23) << 23 == 0 (mod 2^32): one IMAD adds n << 23
+    y0 = __int_as_float(__float_as_int(t0) * (1 << 23) + __float_as_int(p0));
+    y1 = __int_as_float(__float_as_int(t1) * (1 << 23) + __float_as_int(p1));
 }
 
 template <int D>
@@ -139,7 +155,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint8_t *sQ = smem;                                        // 1 tile
     uint8_t *sKV = smem + C::TILE_BYTES;                       // NS tiles
     SmemBars *bars = reinterpret_cast<SmemBars *>(smem + C::SMEM_TILES * C::TILE_BYTES);
-    __shared__ float xml[4 * BM];   // [parity][row]: m, then [2 + parity][row]: l (epilogue merge)
+    __shared__ float xm[BM];            // running max handed from the group of tile j-1 to the group of tile j
+    __shared__ float xml[2 * NG][BM];   // epilogue: [g] = last max seen by group g, [NG + g] = its partial sum
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -154,10 +171,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_init(&bars->kv_full[i], 1);
             ptx::mbar_init(&bars->kv_empty[i], 2);   // released by the MMA issuers of both CTAs of the pair
         }
-        for (int t = 0; t < 2; ++t) {
+        for (int t = 0; t < NG; ++t) {
             ptx::mbar_init(&bars->s_full[t], 1);
-            ptx::mbar_init(&bars->p_full[t][0], 4);   // one arrival per softmax warp of that parity
+            ptx::mbar_init(&bars->p_full[t][0], 4);   // one arrival per softmax warp of that group
             ptx::mbar_init(&bars->p_full[t][1], 4);
+            ptx::mbar_init(&bars->pv_done[t], 1);
         }
         ptx::mbar_init(&bars->o_final, 1);
         ptx::fence_mbar_init();
@@ -179,6 +197,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     if (warp == PRODUCER_WARP) {
         // ------------------------------------------------------------ TMA producer
+        ptx::setmaxnreg_dec<AUX_REGS>();
         const uint64_t pol_q = ptx::policy_evict_first();
         const uint64_t pol_kv = ptx::policy_evict_last();
         if (lane == 0) {
@@ -216,15 +235,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             __syncwarp();
             ++cnt;
         };
-        // same order as the MMA issuer consumes: K0, K1, then V_j, K_{j+2}
-        load(false, 0);
-        if (n_kv > 1) load(false, 1);
+        // same order as the MMA issuer consumes: K0 .. K_{NG-1}, then V_j, K_{j+NG}
+        for (int j = 0; j < NG && j < n_kv; ++j) load(false, j);
         for (int j = 0; j < n_kv; ++j) {
             load(true, j);
-            if (j + 2 < n_kv) load(false, j + 2);
+            if (j + NG < n_kv) load(false, j + NG);
         }
     } else if (warp == MMA_WARP) {
         // ------------------------------------------------------------ MMA issuer
+        ptx::setmaxnreg_dec<AUX_REGS>();
         constexpr uint32_t IDESC_QK = ptx::idesc_bf16(BM, BN, 0, 0);
         constexpr uint32_t IDESC_PV = ptx::idesc_bf16(BM, D, 0, 1);
         const uint32_t qa = ptx::smem_u32(sQ);
@@ -245,12 +264,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         constexpr uint32_t rowb = C::V_ATOM_COLS * 2;
         const uint64_t dV = ptx::smem_desc(sKV_addr, C::V_ATOM_BYTES, 8 * rowb, C::V_SW64 ? 4u : 2u);
         const bool leader = ptx::elect_one();
-        // S(j) = Q K_j^T into S buffer j%2: K-major A (Q) and B (K), 16-element k-steps per swizzle chunk.
+        const uint32_t tO = tmem + C::O_COL;
+        // S(j) = Q K_j^T into S buffer j%NG: K-major A (Q) and B (K), 16-element k-steps per swizzle chunk.
         auto issue_qk = [&](int j) {
             const int slot = acquire();
             if (leader) {
                 const uint64_t so = (uint64_t)(slot * C::TILE_BYTES) >> 4;
-                const uint32_t d = tmem + (j & 1) * 128;
+                const uint32_t d = tmem + (j % NG) * 128;
 #pragma unroll
                 for (int c = 0; c < C::NCHUNK; ++c) {
                     const bool sw64 = (c >= C::N128);
@@ -262,64 +282,66 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                     (c | kk) ? 1u : 0u);
                     }
                 }
-                ptx::mma_commit(&bars->s_full[j & 1]);
+                ptx::mma_commit(&bars->s_full[j % NG]);
                 ptx::mma_commit_mc(&bars->kv_empty[slot], 0x3);
             }
             __syncwarp();
         };
 
         ptx::mbar_wait(&bars->q_full, 0);
-        issue_qk(0);
-        if (n_kv > 1) issue_qk(1);
+        for (int j = 0; j < NG && j < n_kv; ++j) issue_qk(j);
         for (int j = 0; j < n_kv; ++j) {
-            const int t = j & 1;
+            const int t = j % NG;
             const uint32_t tS = tmem + t * 128;
-            const uint32_t tO = tmem + 256 + t * 128;
             const int slotV = acquire();
             const uint64_t dVs = dV + ((uint64_t)(slotV * C::TILE_BYTES) >> 4);
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
-                ptx::mbar_wait(&bars->p_full[t][hf], (j >> 1) & 1);
+                ptx::mbar_wait(&bars->p_full[t][hf], (j / NG) & 1);
                 ptx::tc_fence_after();
                 if (leader) {
                     TRACE(j, hf);
-                    // O_t (+)= P(j)[keys 64hf..64hf+63] V_j[those keys]; that P half sits in columns 64hf..64hf+31
+                    // O (+)= P(j)[keys 64hf..64hf+63] V_j[those keys]; that P half sits in columns 64hf..64hf+31
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const int key16 = hf * 4 + kk;
                         ptx::mma_ts(tO, tS + hf * 64 + kk * 8, dVs + ((uint64_t)(key16 * 16 * rowb) >> 4), IDESC_PV,
-                                    (j >= 2 || key16 > 0) ? 1u : 0u);
+                                    (j > 0 || key16 > 0) ? 1u : 0u);
                     }
                     if (hf == 1) {
                         ptx::mma_commit_mc(&bars->kv_empty[slotV], 0x3);
+                        ptx::mma_commit(&bars->pv_done[t]);
                         if (j == n_kv - 1) ptx::mma_commit(&bars->o_final);
                     }
                 }
                 __syncwarp();
             }
-            if (j + 2 < n_kv) issue_qk(j + 2);
+            if (j + NG < n_kv) issue_qk(j + NG);
         }
-    } else {
+    } else if (warp < NUM_SOFTMAX_WARPS) {
         // ------------------------------------------------------------ softmax / correction / epilogue
-        const int t = warp >> 2;                       // tile parity handled by this warp
+        ptx::setmaxnreg_inc<SOFTMAX_REGS>();
+        const int g = warp >> 2;                       // softmax group: KV tiles j with j % NG == g
         const int wq = warp & 3;                       // TMEM lane quarter this warp may access (= SMSP)
         const int row = wq * 32 + lane;                // row within the tile
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-        const uint32_t tS = tmem + lane_base + t * 128;
-        const uint32_t tO = tmem + lane_base + 256 + t * 128;
+        const uint32_t tS = tmem + lane_base + g * 128;
+        const uint32_t tO = tmem + lane_base + C::O_COL;
         const float sl2 = args.scale_log2;
         const uint64_t SL2 = ptx::f2pack(sl2, sl2);
         const int last_valid = args.Skv - (n_kv - 1) * BN;   // valid keys in the last tile (1..128)
         const bool tr = (lane == 0 && wq == 0);
+        const uint32_t bar_in = 1 + 3 * wq + g;                  // "m of tile j-1 is in xm[]" for this warp
+        const uint32_t bar_out = 1 + 3 * wq + (g + 1) % NG;      // ... for the warp of the next group
 
-        float m = -INFINITY;   // running max of this parity's tiles, scaled to the log2 domain
-        float l = 0.f;         // running sum of p of this parity's tiles (fp32)
-        for (int j = t; j < n_kv; j += 2) {
+        float mg = -INFINITY;  // the running max this group last used (its l is relative to it)
+        float l = 0.f;         // this group's partial row sum (fp32)
+        for (int j = g; j < n_kv; j += NG) {
             const bool masked = (j == n_kv - 1) && (last_valid < BN);
-            if (tr) TRACE(j, 3 + 5 * t);
-            ptx::mbar_wait(&bars->s_full[t], (j >> 1) & 1);
+            if (tr) TRACE(j, 3);
+            ptx::mbar_wait(&bars->s_full[g], (j / NG) & 1);
             ptx::tc_fence_after();
-            if (tr) TRACE(j, 4 + 5 * t);
+            if (tr) TRACE(j, 4);
             // pass 1: row max over the 128 keys, two rounds of 64 columns (keeps registers low)
             float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
 #pragma unroll
@@ -344,27 +366,42 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
             }
             const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl2;
-            if (tr) TRACE(j, 5 + 5 * t);
-            const bool resc = mx > m + RESCALE_TAU;   // also true on this parity's first tile (m = -inf)
-            if (__any_sync(0xffffffffu, resc)) {
-                float factor = 1.f;
-                if (resc) {
-                    factor = ptx::ex2(m - mx);        // 0 on the first tile
-                    m = mx;
-                }
-                l *= factor;
-                // O_t *= factor for the moved rows (others by exactly 1).  PV(j-2), the last product into
-                // O_t, completed before S(j) did (it was issued first), and PV(j) waits for this P.
-                if (j >= 2) {
+            // running max after tile j-1, handed over by the previous group (strict tile order)
+            float mprev = -INFINITY;
+            if (j > 0) {
+                ptx::named_bar_sync(bar_in, 64);
+                mprev = xm[row];
+            }
+            const bool resc = mx > mprev + RESCALE_TAU;   // also true on tile 0 (mprev = -inf)
+            const float m = resc ? mx : mprev;
+            if (j + 1 < n_kv) {
+                xm[row] = m;
+                __threadfence_block();
+                ptx::named_bar_arrive(bar_out, 64);
+            }
+            if (tr) TRACE(j, 5);
+            if (m != mg) {   // this group's partial sum follows the reference max
+                l *= ptx::ex2(mg - m);   // mg = -inf: l = 0 anyway
+                mg = m;
+            }
+            if (j > 0 && __any_sync(0xffffffffu, resc)) {
+                // O *= 2^(mprev - m) for the moved rows (others by exactly 1), after PV(j-1), the last product
+                // into O, completed; PV(j) waits for this P.
+                const float factor = resc ? ptx::ex2(mprev - m) : 1.f;
+                // PV(j-1) is completion jp/NG of pv_done[jp%NG].  The parity test is unambiguous: PV(j-4) was
+                // committed before S(j-1), which the previous group saw complete before handing over the max,
+                // and PV(j+2) cannot complete before PV(j), which needs this group's P(j).
+                const int jp = j - 1;
+                ptx::mbar_wait(&bars->pv_done[jp % NG], (jp / NG) & 1);
+                ptx::tc_fence_after();
 #pragma unroll
-                    for (int c = 0; c < D / 32; ++c) {
-                        uint32_t r[32];
-                        ptx::tmem_ld32(tO + 32 * c, r);
-                        ptx::tmem_wait_ld();
+                for (int c = 0; c < D / 32; ++c) {
+                    uint32_t r[32];
+                    ptx::tmem_ld32(tO + 32 * c, r);
+                    ptx::tmem_wait_ld();
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * factor);
-                        ptx::tmem_st32(tO + 32 * c, r);
-                    }
+                    for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * factor);
+                    ptx::tmem_st32(tO + 32 * c, r);
                 }
             }
             // pass 2, per 64-key half: reload the scores, P = exp2(s*sl2 - m) in f32x2 pairs (MUFU or FMA-pipe
@@ -409,7 +446,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ptx::tmem_wait_st();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&bars->p_full[t][h]);
+                if (lane == 0) ptx::mbar_arrive(&bars->p_full[g][h]);
             }
             {
                 float a0, a1, b0, b1;
@@ -417,48 +454,47 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ptx::f2unpack(L1, b0, b1);
                 l += (a0 + b0) + (a1 + b1);
             }
-            if (tr) TRACE(j, 6 + 5 * t);
+            if (tr) TRACE(j, 6);
         }
-        // ------------------------------------------------------------ epilogue: merge parities, O / l -> global
-        xml[t * BM + row] = m;
-        xml[(2 + t) * BM + row] = l;
-        ptx::named_bar_sync(1 + wq, 64);               // the two parity warps of this lane quarter
-        const float me = xml[row], mo = xml[BM + row];
-        const float mm = fmaxf(me, mo);
-        const float se = (me == -INFINITY) ? 0.f : ptx::ex2(me - mm);   // odd parity may have no tile (n_kv = 1)
-        const float so = (mo == -INFINITY) ? 0.f : ptx::ex2(mo - mm);
-        const float inv = 1.f / (xml[2 * BM + row] * se + xml[3 * BM + row] * so);
-        const float ce = se * inv, co = so * inv;
+        // ------------------------------------------------------------ epilogue: merge group sums, O / l -> global
+        xml[g][row] = mg;
+        xml[NG + g][row] = l;
+        ptx::named_bar_sync(BAR_EPI, 32 * NUM_SOFTMAX_WARPS);
+        float mm = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < NG; ++q) mm = fmaxf(mm, xml[q][row]);   // = the max after the last tile, O's reference
+        float lsum = 0.f;
+#pragma unroll
+        for (int q = 0; q < NG; ++q) {
+            const float mq = xml[q][row];
+            if (mq != -INFINITY) lsum += xml[NG + q][row] * ptx::ex2(mq - mm);   // a group may have no tile
+        }
+        const float inv = 1.f / lsum;
         ptx::mbar_wait(&bars->o_final, 0);
         ptx::tc_fence_after();
         const long long srow = (long long)qtile * BM + row;
         const bool valid = srow < args.Sq;      // tcgen05.ld is warp-collective: every lane loads, valid lanes store
         uint4 *dst = reinterpret_cast<uint4 *>(args.O + (long long)b * args.o_batch_stride + srow * args.o_tok_stride +
                                                (long long)head * D);
-        // this warp merges and stores O columns [t*DH, t*DH + DH) in chunks of 16
-        const uint32_t tOe = tmem + lane_base + 256, tOo = tmem + lane_base + 384;
+        // this warp normalises and stores the 16-column chunks c with c % NG == g
 #pragma unroll
-        for (int c = 0; c < C::DH / 16; ++c) {
-            const int col = t * C::DH + 16 * c;
-            uint32_t re[16], ro[16];
-            ptx::tmem_ld16(tOe + col, re);
-            if (n_kv > 1) ptx::tmem_ld16(tOo + col, ro);   // O_odd is never written when n_kv == 1
+        for (int c = 0; c < C::OCHUNKS; ++c) {
+            if (c % NG != g) continue;
+            const int col = 16 * c;
+            uint32_t r[16];
+            ptx::tmem_ld16(tO + col, r);
             ptx::tmem_wait_ld();
             uint32_t w[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                float v0 = __uint_as_float(re[2 * u]) * ce, v1 = __uint_as_float(re[2 * u + 1]) * ce;
-                if (n_kv > 1) {
-                    v0 = fmaf(__uint_as_float(ro[2 * u]), co, v0);
-                    v1 = fmaf(__uint_as_float(ro[2 * u + 1]), co, v1);
-                }
-                w[u] = ptx::pack_bf16x2(v0, v1);
-            }
+            for (int u = 0; u < 8; ++u)
+                w[u] = ptx::pack_bf16x2(__uint_as_float(r[2 * u]) * inv, __uint_as_float(r[2 * u + 1]) * inv);
             if (valid) {
                 dst[col / 8] = make_uint4(w[0], w[1], w[2], w[3]);
                 dst[col / 8 + 1] = make_uint4(w[4], w[5], w[6], w[7]);
             }
         }
+    } else {
+        ptx::setmaxnreg_dec<AUX_REGS>();   // idle warps of the last warpgroup
     }
     ptx::tc_fence_before();
     __syncthreads();
