@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         auto issue_qk = [&](int j) {
             const int slot = acquire();
             if (leader) {
+                TRACE(j, 2);
                 const uint64_t so = (uint64_t)(slot * C::TILE_BYTES) >> 4;
                 const uint32_t d = tmem + (j % NG) * 128;
 #pragma unroll
@@ -294,6 +295,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int t = j % NG;
             const uint32_t tS = tmem + t * 128;
             const int slotV = acquire();
+            if (leader) TRACE(j, 10);
             const uint64_t dVs = dV + ((uint64_t)(slotV * C::TILE_BYTES) >> 4);
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
@@ -366,6 +368,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
             }
             const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl2;
+            if (tr) TRACE(j, 7);
             // running max after tile j-1, handed over by the previous group (strict tile order)
             float mprev = -INFINITY;
             if (j > 0) {
@@ -447,6 +450,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&bars->p_full[g][h]);
+                if (tr && h == 0) TRACE(j, 8);
             }
             {
                 float a0, a1, b0, b1;

@@ -1,11 +1,14 @@
 #!/usr/bin/env python
 """Per-iteration timeline of one attention CTA (debug build lib/libspa_trace.so, SPA_ATTN_TRACE).
 
+    python -m paper_2511_12056_b200._build --trace
     SPA_LIB=paper_2511_12056_b200/lib/libspa_trace.so python tools/attn_trace.py [--D 128]
 Events (clock64 cycles) per KV iteration j of CTA (0,0,0):
-  0/1  MMA issuer: P(j) key-half 0/1 ready (PV half issued)
-  3/8  softmax key-half 0/1 (quarter-0 warp): before waiting for S(j)
-  4/9  S(j) ready     5/10 row max exchanged     6/11 P half written and released
+  MMA issuer (elected lane):  2 K_j acquired -> QK(j) issued   10 V_j acquired
+                              0 / 1  P(j) key-half 0 / 1 ready -> PV half issued
+  softmax, lane 0 of the lane-quarter-0 warp of group j % NG:
+                              3 loop top (before waiting for S(j))   4 S(j) ready   7 pass-1 max done
+                              5 running max handed over              8 P half 0 released   6 P half 1 released
 """
 import argparse
 import ctypes
@@ -24,6 +27,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--D", type=int, default=128)
 ap.add_argument("--S", type=int, default=32768)
 ap.add_argument("--H", type=int, default=8)
+ap.add_argument("--rows", type=int, default=12)
 args = ap.parse_args()
 lib = spa.load()
 q, k, v = (synthgen.gen_qkv_shard(0, t, (1, args.S, args.H, args.D), 0, args.S, device="cuda") for t in range(3))
@@ -34,21 +38,22 @@ buf = (ctypes.c_ulonglong * (256 * 16))()
 lib.spa_debug_read_trace.argtypes = [ctypes.c_void_p]
 assert lib.spa_debug_read_trace(ctypes.addressof(buf)) == 0
 T = np.frombuffer(buf, dtype=np.uint64).reshape(256, 16).astype(np.int64)
-t0 = T[0, 3]
 n = min(256, (args.S + 127) // 128)
-print("  j | mma: P0rdy   P1rdy | sm0: wait  Srdy   maxx   Pdone | sm1: wait  Srdy   maxx   Pdone")
-for j in list(range(0, 8)) + list(range(n // 2, n // 2 + 4)) + list(range(n - 3, n)):
+t0 = T[0, 2]
+print("   j |  QKiss  Vacq   P0rdy   P1rdy |  top    Srdy   max    xchg   P0rel  P1rel")
+mid0 = n // 2
+for j in list(range(0, args.rows)) + list(range(mid0, mid0 + 6)) + list(range(n - 3, n)):
     r = T[j] - t0
-    print(f"{j:3d} | {r[0]:8d} {r[1]:8d} | {r[3]:8d} {r[4]:8d} {r[5]:8d} {r[6]:8d} | {r[8]:8d} {r[9]:8d} {r[10]:8d} {r[11]:8d}"
-          f" | qk: acq {r[12]:8d} got {r[13]:8d} | V: acq {r[14]:8d} got {r[15]:8d} | load K {r[2]:8d} V {r[7]:8d}")
-mid = slice(n // 4, 3 * n // 4)
-d = T[mid]
-per = np.diff(d[:, 1]).mean()
-ideal = {128: 1024, 96: 768, 64: 512}[args.D]
-print(f"steady-state period per KV tile: {per:.0f} cycles (MMA-bound ideal {ideal} at D={args.D})")
-# softmax events of tile j are written by the warps of tile parity j % 2 (base 3 or 8)
+    print(f"{j:4d} | {r[2]:7d} {r[10]:7d} {r[0]:7d} {r[1]:7d} | {r[3]:7d} {r[4]:7d} {r[7]:7d} {r[5]:7d} {r[8]:7d} {r[6]:7d}")
 js = np.arange(n // 4, 3 * n // 4)
-ev = np.stack([T[j, 3 + 5 * (j % 2): 7 + 5 * (j % 2)] for j in js])   # [tiles, 4]: loop top, S ready, max, P done
-print(f"per tile (its parity's warps): wait S {np.mean(ev[:, 1] - ev[:, 0]):.0f}  max {np.mean(ev[:, 2] - ev[:, 1]):.0f}  "
-      f"exp+store {np.mean(ev[:, 3] - ev[:, 2]):.0f}  (a parity handles every other tile)")
-print(f"MMA: P(j) ready -> P(j+1) ready {np.mean(np.diff(T[js, 1])):.0f} cycles")
+d = T[js]
+ideal = {128: 1024, 96: 768, 64: 512}[args.D]
+print(f"steady-state period per KV tile: {np.diff(d[:, 1]).mean():.0f} cycles (P1 ready to P1 ready; "
+      f"MMA-bound ideal {ideal} at D={args.D})")
+print("per tile, mean cycles: "
+      f"wait S {np.mean(d[:, 4] - d[:, 3]):.0f} | pass1 {np.mean(d[:, 7] - d[:, 4]):.0f} | "
+      f"xchg {np.mean(d[:, 5] - d[:, 7]):.0f} | half0 {np.mean(d[:, 8] - d[:, 5]):.0f} | "
+      f"half1 {np.mean(d[:, 6] - d[:, 8]):.0f} | softmax busy {np.mean(d[:, 6] - d[:, 4]):.0f}")
+print("MMA side: "
+      f"QK(j) issue -> P0(j) ready {np.mean(d[:, 0] - d[:, 2]):.0f} | P0 -> P1 {np.mean(d[:, 1] - d[:, 0]):.0f} | "
+      f"S(j) ready - QK(j) issue {np.mean(d[:, 4] - d[:, 2]):.0f}")
