@@ -47,6 +47,10 @@ def _load():
         lib.oracle_attention_rows.restype = ctypes.c_int
         lib.oracle_softmax_weights.argtypes = [dp, dp, ctypes.c_long, ctypes.c_long, dp]
         lib.oracle_softmax_weights.restype = ctypes.c_int
+        u8p = ctypes.POINTER(ctypes.c_ubyte)
+        lib.oracle_attention_rows_masked.argtypes = [dp, ctypes.c_long, ctypes.c_long, dp, dp, ctypes.c_long,
+                                                     ctypes.c_long, u8p, dp, ctypes.c_long, ctypes.c_int]
+        lib.oracle_attention_rows_masked.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -66,17 +70,28 @@ def default_threads() -> int:
     return os.cpu_count() or 1
 
 
-def attention_rows(q: np.ndarray, K: np.ndarray, V: np.ndarray, nthreads: Optional[int] = None) -> np.ndarray:
-    """q [R,D], K [S,D], V [S,D] (float64) -> [R,D] float64."""
+def attention_rows(q: np.ndarray, K: np.ndarray, V: np.ndarray, nthreads: Optional[int] = None,
+                   key_valid: Optional[np.ndarray] = None) -> np.ndarray:
+    """q [R,D], K [S,D], V [S,D] (float64) -> [R,D] float64.
+
+    key_valid: optional [S] bool key-padding mask (Alg. 1's attention_mask; DESIGN.md
+    R20): masked keys take no part in the softmax; a row with no valid key is 0."""
     q, K, V = _f64c(q), _f64c(K), _f64c(V)
     if q.ndim == 1:
-        return attention_rows(q[None], K, V, nthreads)[0]
+        return attention_rows(q[None], K, V, nthreads, key_valid)[0]
     R, D = q.shape
     S = K.shape[0]
     assert K.shape == (S, D) and V.shape == (S, D)
     out = np.empty((R, D), dtype=np.float64)
-    rc = _load().oracle_attention_rows(_dptr(q), R, D, _dptr(K), _dptr(V), S, D, _dptr(out), D,
-                                       int(nthreads or default_threads()))
+    nt = int(nthreads or default_threads())
+    if key_valid is None:
+        rc = _load().oracle_attention_rows(_dptr(q), R, D, _dptr(K), _dptr(V), S, D, _dptr(out), D, nt)
+    else:
+        kv = np.ascontiguousarray(np.asarray(key_valid, dtype=bool).astype(np.uint8))
+        assert kv.shape == (S,)
+        rc = _load().oracle_attention_rows_masked(_dptr(q), R, D, _dptr(K), _dptr(V), S, D,
+                                                  kv.ctypes.data_as(ctypes.POINTER(ctypes.c_ubyte)), _dptr(out),
+                                                  D, nt)
     if rc != 0:
         raise RuntimeError(f"oracle_attention_rows failed ({rc})")
     return out
@@ -92,13 +107,23 @@ def softmax_weights(q: np.ndarray, K: np.ndarray) -> np.ndarray:
     return w
 
 
-def mha_unsharded(Q: np.ndarray, K: np.ndarray, V: np.ndarray, nthreads: Optional[int] = None) -> np.ndarray:
-    """Full multi-head attention on unsharded [B,S,H,D] float64 tensors (per head, per batch)."""
+def mha_unsharded(Q: np.ndarray, K: np.ndarray, V: np.ndarray, nthreads: Optional[int] = None,
+                  key_valid: Optional[np.ndarray] = None) -> np.ndarray:
+    """Full multi-head attention on unsharded [B,S,H,D] float64 tensors (per head, per batch).
+
+    key_valid: optional [B,S] bool key-padding mask (the same for every head of a batch entry)."""
     B, S, H, D = Q.shape
     out = np.empty((B, S, H, D), dtype=np.float64)
     for b in range(B):
+        kv = None if key_valid is None else np.asarray(key_valid)[b]
         for k in range(H):
             out[b, :, k, :] = attention_rows(np.ascontiguousarray(Q[b, :, k, :]),
                                              np.ascontiguousarray(K[b, :, k, :]),
-                                             np.ascontiguousarray(V[b, :, k, :]), nthreads)
+                                             np.ascontiguousarray(V[b, :, k, :]), nthreads, kv)
     return out
+
+
+def key_valid_from_lengths(kv_len, S: int) -> np.ndarray:
+    """[B,S] bool mask of a key-padding length vector: key t of batch b is valid iff t < kv_len[b]."""
+    kv_len = np.asarray(kv_len, dtype=np.int64)
+    return np.arange(S)[None, :] < kv_len[:, None]

@@ -32,32 +32,48 @@
 #include <stdlib.h>
 #include <string.h>
 
-/* softmax weights w[t] = e[t]/l of one row (exported for the row-sum pins). */
-int oracle_softmax_weights(const double *q, const double *K, long S, long D, double *w)
+/*
+ * Softmax weights w[t] = e[t]/l of one row.  key_valid (NULL = every key valid) is the key-padding
+ * mask of Alg. 1's `attention(Q[:,j], K[:,j], V[:,j], attention_mask[:,j])` (the
+ * paper never defines it -- DESIGN.md reading R2/R20): a masked key takes no part in the softmax,
+ * i.e. z[t] = -inf, e[t] = 0.  A row with no valid key gets w = 0 everywhere (its output is 0).
+ */
+int oracle_softmax_weights_masked(const double *q, const double *K, long S, long D, const unsigned char *key_valid,
+                                  double *w)
 {
     if (!q || !K || !w || S <= 0 || D <= 0) return 1;
     double sqrt_d = sqrt((double)D);
     double m = -INFINITY;
     for (long t = 0; t < S; ++t) {
+        if (key_valid && !key_valid[t]) { w[t] = -INFINITY; continue; }
         double acc = 0.0;
         for (long d = 0; d < D; ++d) acc += q[d] * K[t * D + d];
         w[t] = acc / sqrt_d;
         if (w[t] > m) m = w[t];
     }
+    if (m == -INFINITY) {           /* no valid key */
+        for (long t = 0; t < S; ++t) w[t] = 0.0;
+        return 0;
+    }
     double l = 0.0;
     for (long t = 0; t < S; ++t) {
-        w[t] = exp(w[t] - m);
+        w[t] = (w[t] == -INFINITY) ? 0.0 : exp(w[t] - m);
         l += w[t];
     }
     for (long t = 0; t < S; ++t) w[t] = w[t] / l;
     return 0;
 }
 
+int oracle_softmax_weights(const double *q, const double *K, long S, long D, double *w)
+{
+    return oracle_softmax_weights_masked(q, K, S, D, NULL, w);
+}
+
 /* One output row: out[D] = sum_t w[t] V[t,:] (t ascending). scratch has S doubles. */
 static void attention_one_row(const double *q, const double *K, const double *V, long S, long D,
-                              double *out, double *scratch)
+                              const unsigned char *key_valid, double *out, double *scratch)
 {
-    oracle_softmax_weights(q, K, S, D, scratch);
+    oracle_softmax_weights_masked(q, K, S, D, key_valid, scratch);
     for (long d = 0; d < D; ++d) out[d] = 0.0;
     for (long t = 0; t < S; ++t) {
         double wt = scratch[t];
@@ -68,6 +84,7 @@ static void attention_one_row(const double *q, const double *K, const double *V,
 
 typedef struct {
     const double *Q, *K, *V;
+    const unsigned char *key_valid;
     double *O;
     long nq, S, D;
     long q_stride, o_stride; /* elements between consecutive query / output rows */
@@ -81,18 +98,20 @@ static void *rows_worker(void *arg)
     double *scratch = (double *)malloc(sizeof(double) * (size_t)j->S);
     if (!scratch) { j->err = 2; return NULL; }
     for (long r = j->tid; r < j->nq; r += j->nthreads)
-        attention_one_row(j->Q + r * j->q_stride, j->K, j->V, j->S, j->D, j->O + r * j->o_stride, scratch);
+        attention_one_row(j->Q + r * j->q_stride, j->K, j->V, j->S, j->D, j->key_valid, j->O + r * j->o_stride,
+                          scratch);
     free(scratch);
     return NULL;
 }
 
 /*
- * out[r][:] = attention(Q[r][:], K, V) for r < nq.
- * Q rows at stride q_stride, out rows at o_stride; K, V dense [S][D].
+ * out[r][:] = attention(Q[r][:], K, V) for r < nq, over the keys with key_valid[t] != 0
+ * (key_valid NULL = all keys).  Q rows at stride q_stride, out rows at o_stride; K, V dense [S][D].
  * nthreads <= 0 -> 1.  Returns 0 on success.
  */
-int oracle_attention_rows(const double *Q, long nq, long q_stride, const double *K, const double *V,
-                          long S, long D, double *out, long o_stride, int nthreads)
+int oracle_attention_rows_masked(const double *Q, long nq, long q_stride, const double *K, const double *V,
+                                 long S, long D, const unsigned char *key_valid, double *out, long o_stride,
+                                 int nthreads)
 {
     if (!Q || !K || !V || !out || S <= 0 || D <= 0 || nq < 0) return 1;
     if (nthreads <= 0) nthreads = 1;
@@ -101,7 +120,7 @@ int oracle_attention_rows(const double *Q, long nq, long q_stride, const double 
     pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
     if (!jobs || !th) { free(jobs); free(th); return 2; }
     for (int i = 0; i < nthreads; ++i) {
-        jobs[i] = (rows_job){Q, K, V, out, nq, S, D, q_stride, o_stride, i, nthreads, 0};
+        jobs[i] = (rows_job){Q, K, V, key_valid, out, nq, S, D, q_stride, o_stride, i, nthreads, 0};
         if (nthreads == 1) rows_worker(&jobs[i]);
         else pthread_create(&th[i], NULL, rows_worker, &jobs[i]);
     }
@@ -113,4 +132,10 @@ int oracle_attention_rows(const double *Q, long nq, long q_stride, const double 
     free(jobs);
     free(th);
     return err;
+}
+
+int oracle_attention_rows(const double *Q, long nq, long q_stride, const double *K, const double *V,
+                          long S, long D, double *out, long o_stride, int nthreads)
+{
+    return oracle_attention_rows_masked(Q, nq, q_stride, K, V, S, D, NULL, out, o_stride, nthreads);
 }

@@ -126,6 +126,22 @@ def pad_heads(H: int, n: int) -> Tuple[int, int]:
     return Hp, Hp - H
 
 
+def padded_forward(Qs, Ks, Vs, n_owners: int, forward) -> List[np.ndarray]:
+    """Head padding ("padding increases the head count to 28 so that each GPU
+    handles 4 heads"): append pad_heads(H, n_owners)[1] all-zero heads to every shard's Q, K, V, run
+    `forward(Qs', Ks', Vs')` (e.g. ulysses_forward / pipesp_forward) on the padded problem, and drop
+    the pad heads from every output shard.  Heads are independent, so the real heads'
+    result is the unpadded one; a zero pad head attends with uniform weights to zero values -> 0."""
+    B, S_l, H, D = Qs[0].shape
+    Hp, n_pad = pad_heads(H, n_owners)
+    if n_pad == 0:
+        return forward(Qs, Ks, Vs)
+    padz = np.zeros((B, S_l, n_pad, D), dtype=np.float64)
+    pad = lambda xs: [np.concatenate([x, padz], axis=2) for x in xs]  # noqa: E731
+    outs = forward(pad(Qs), pad(Ks), pad(Vs))
+    return [np.ascontiguousarray(o[:, :, :H]) for o in outs]
+
+
 # ---------------------------------------------------------------- attention per rank
 def _attn_heads(Rq: np.ndarray, Rk: np.ndarray, Rv: np.ndarray, rows: np.ndarray, heads: Sequence[int],
                 attn: Attn) -> np.ndarray:
