@@ -45,10 +45,12 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
-    """trace=True builds lib/libspa_trace.so with the attention timeline hooks (tools/attn_trace.py)."""
-    out_lib = TRACE_LIB if trace else LIB
-    if not force and not trace and not _stale():
+def build(force: bool = False, verbose: bool = False, trace: bool = False, variant: str = "",
+          defines: tuple = ()) -> str:
+    """trace=True builds lib/libspa_trace.so with the attention timeline hooks (tools/attn_trace.py);
+    variant="x" with defines=("-DNAME=V", ...) builds lib/libspa_x.so (tuning sweeps, tools/variants.py)."""
+    out_lib = TRACE_LIB if trace else (os.path.join(LIBDIR, f"libspa_{variant}.so") if variant else LIB)
+    if not force and not trace and not variant and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     inc, lib = nccl_dirs()
@@ -57,8 +59,10 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
               f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}", "-Xptxas", "-v" if verbose else "-O3"]
     if trace:
         common = common + ["-DSPA_ATTN_TRACE"]
+    common = common + list(defines)
     for src in SOURCES:
-        obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + (".trace.o" if trace else ".o"))
+        tag = ".trace" if trace else (f".{variant}" if variant else "")
+        obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + tag + ".o")
         cmd = common + ["-x", "cu" if src.endswith(".cu") else "c++", "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cpp"):
             cmd = [nvcc(), "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O3", f"-I{inc}",

@@ -21,8 +21,8 @@
 //     O in TMEM before releasing P(j).  Each group keeps its own partial row sum l_g relative to the last
 //     max it saw; the epilogue merges them.
 //   warp 12 TMA producer (warps 13, 14 idle): Q once, then K/V tiles through an NS-slot smem ring in consumption order
-//           (K0, K1, K2, V0, K3, V1, K4, ...); each CTA of the pair fetches 64 of the 128 rows of every tile
-//           and multicasts them to both CTAs.
+//           (K0, K1, K2, V0, K3, V1, K4, ...); each CTA of the cluster (CL CTAs) fetches 128/CL of the rows of
+//           every tile and multicasts them to all of them.
 //   warp 15 TMEM allocator + tcgen05.mma issuer (one elected lane; highest warp id = scheduler priority):
 //           S(j) = Q K_j^T (SS, M=N=128) into S buffer j%3; O += P(j) V_j (TS: P from TMEM, V MN-major,
 //           N = D in one instruction), released in two key halves; S(j+3) is issued right after PV(j).
@@ -60,7 +60,16 @@ constexpr int MMA_WARP = NUM_SOFTMAX_WARPS + 3;
 constexpr int NUM_WARPS = NUM_SOFTMAX_WARPS + 4;
 constexpr int NUM_THREADS = NUM_WARPS * 32;
 constexpr int SOFTMAX_REGS = 152, AUX_REGS = 56;
-constexpr float RESCALE_TAU = 8.0f;  // log2 domain: raise the running max only if it grows by > 2^8
+constexpr float RESCALE_TAU = 8.0f;
+// CTAs per cluster: adjacent query tiles of one head; each CTA fetches 1/CL of the rows of every K/V tile and
+// multicasts them to the whole cluster (L2->SMEM traffic per query row / CL).
+#ifdef SPA_CLUSTER
+constexpr int CL = SPA_CLUSTER;
+#else
+constexpr int CL = 2;
+#endif
+static_assert(CL == 1 || CL == 2 || CL == 4, "cluster size");
+constexpr uint16_t CL_MASK = (uint16_t)((1u << CL) - 1);  // log2 domain: raise the running max only if it grows by > 2^8
 // named barriers: 0 = __syncthreads; 1 + 3*wq + g = "running max of the previous tile is in xm[] for the
 // warp of group g on lane quarter wq"; 1 + 3*4 = all softmax warps (epilogue merge).
 constexpr uint32_t BAR_EPI = 1 + 3 * 4;
@@ -92,22 +101,30 @@ struct Cfg {
     static constexpr int V_ATOMS = D / V_ATOM_COLS;
     static constexpr int V_ATOM_BYTES = BM * V_ATOM_COLS * 2;
     static constexpr int TILE_BYTES = BM * D * 2;
-    static constexpr int NS = (D == 128) ? 5 : (D == 96 ? 7 : 8);   // K/V ring slots
+    // K/V ring slots (as many as fit: the ring depth is the TMA lookahead that hides L2 latency)
+#if defined(SPA_NS128) && defined(SPA_NS96)
+    static constexpr int NS = (D == 128) ? SPA_NS128 : (D == 96 ? SPA_NS96 : 8);
+#else
+    static constexpr int NS = (D == 128) ? 6 : 8;
+#endif
     static constexpr int SMEM_TILES = 1 + NS;
     static constexpr int BAR_BYTES = 512;
-    static constexpr int XCH_BYTES = (1 + 2 * NG) * BM * 4;   // static smem: running max + per-group (m, l)
+    static constexpr int XCH_BYTES = BM * 4;   // static smem: running max (the epilogue's (m, l) reuse ring slot 0)
     static constexpr int SMEM_BYTES = 1024 /*align slack*/ + SMEM_TILES * TILE_BYTES + BAR_BYTES;
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr uint32_t O_COL = 128 * NG;          // O accumulator columns [O_COL, O_COL + D)
     static_assert(O_COL + D <= TMEM_COLS, "TMEM budget");
     static constexpr int OCHUNKS = D / 16;               // epilogue: 16-column chunks, chunk c by group c % NG
-    // exp2 split: key pairs with (i & 7) >= POLY_FROM use the FMA-pipe polynomial, the rest MUFU.EX2.
+    // exp2 split: key pairs with (key & 15) >= POLY_FROM use the FMA-pipe polynomial, the rest MUFU.EX2
+    // (POLY_FROM = 12: a quarter of the keys on the FMA pipe; 16: none).
 #ifdef SPA_POLY_FROM
     static constexpr int POLY_FROM = SPA_POLY_FROM;
 #else
-    static constexpr int POLY_FROM = 6;
+    static constexpr int POLY_FROM = 12;
 #endif
     static_assert(SMEM_BYTES + XCH_BYTES <= 227 * 1024, "shared memory");
+    static_assert(NS <= 8, "barrier block");
+    static_assert(2 * NG * BM * 4 <= TILE_BYTES, "epilogue exchange fits in a ring slot");
 };
 
 __device__ __forceinline__ int chunk_off(int c) { return c * (BM * 128); }  // Q/K chunk c byte offset in a tile
@@ -156,7 +173,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint8_t *sKV = smem + C::TILE_BYTES;                       // NS tiles
     SmemBars *bars = reinterpret_cast<SmemBars *>(smem + C::SMEM_TILES * C::TILE_BYTES);
     __shared__ float xm[BM];            // running max handed from the group of tile j-1 to the group of tile j
-    __shared__ float xml[2 * NG][BM];   // epilogue: [g] = last max seen by group g, [NG + g] = its partial sum
+    // epilogue: xml[g] = last max seen by group g, xml[NG + g] = its partial sum; in ring slot 0, which is idle once
+    // every MMA of this CTA completed (o_final): all loads into this CTA's ring were consumed by then.
+    float (*xml)[BM] = reinterpret_cast<float (*)[BM]>(sKV);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -169,7 +188,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mbar_init(&bars->q_full, 1);
         for (int i = 0; i < C::NS; ++i) {
             ptx::mbar_init(&bars->kv_full[i], 1);
-            ptx::mbar_init(&bars->kv_empty[i], 2);   // released by the MMA issuers of both CTAs of the pair
+            ptx::mbar_init(&bars->kv_empty[i], CL);   // released by the MMA issuers of every CTA of the cluster
         }
         for (int t = 0; t < NG; ++t) {
             ptx::mbar_init(&bars->s_full[t], 1);
@@ -193,7 +212,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::cluster_sync();   // the partner's barriers exist before any multicast lands in its shared memory
     ptx::tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
-    const uint32_t crank = ptx::cluster_ctarank();   // which half (64 rows) of each K/V tile this CTA fetches
+    const uint32_t crank = CL > 1 ? ptx::cluster_ctarank() : 0;   // which 128/CL rows of each K/V tile it fetches
 
     if (warp == PRODUCER_WARP) {
         // ------------------------------------------------------------ TMA producer
@@ -207,8 +226,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (C::N64) ptx::tma_load_4d(&tmQb, &bars->q_full, sQ + chunk_off(1), 64, head, qtile * BM, b, pol_q);
         }
         int cnt = 0;
-        // Each CTA of the pair fetches rows [64*crank, 64*crank+64) of every K/V tile and multicasts them to
-        // both CTAs (same smem offset); each CTA's kv_full expects the whole tile.
+        // Each CTA of the cluster fetches rows [crank*RB, crank*RB + RB) of every K/V tile and multicasts them to
+        // all CTAs (same smem offset); each CTA's kv_full expects the whole tile.
+        constexpr int RB = BN / CL;
+        auto tload = [&](const CUtensorMap *m, uint64_t *bar, uint8_t *dst, int c0, int row) {
+            if (CL == 1) ptx::tma_load_4d(m, bar, dst, c0, head, row, b, pol_kv);
+            else ptx::tma_load_4d_mc(m, bar, dst, c0, head, row, b, CL_MASK, pol_kv);
+        };
         auto load = [&](bool isV, int j) {
             const int slot = cnt % C::NS;
             ptx::mbar_wait(&bars->kv_empty[slot], ((cnt / C::NS) & 1) ^ 1);
@@ -216,20 +240,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 uint8_t *dst = sKV + slot * C::TILE_BYTES;
                 uint64_t *bar = &bars->kv_full[slot];
                 ptx::mbar_arrive_expect_tx(bar, C::TILE_BYTES);
-                const int row = j * BN + (int)crank * (BN / 2);
+                TRACE(j, isV ? 12 : 11);
+                const int row = j * BN + (int)crank * RB;
                 if (isV) {
 #pragma unroll
                     for (int a = 0; a < C::V_ATOMS; ++a)
-                        ptx::tma_load_4d_mc(&tmVa, bar, dst + a * C::V_ATOM_BYTES + crank * (C::V_ATOM_BYTES / 2),
-                                            a * C::V_ATOM_COLS, head, row, b, 0x3, pol_kv);
+                        tload(&tmVa, bar, dst + a * C::V_ATOM_BYTES + crank * (C::V_ATOM_BYTES / CL), a * C::V_ATOM_COLS,
+                              row);
                 } else {
-                    ptx::tma_load_4d_mc(&tmKa, bar, dst + crank * (BM / 2) * 128, 0, head, row, b, 0x3, pol_kv);
-                    if (C::N128 == 2)
-                        ptx::tma_load_4d_mc(&tmKa, bar, dst + chunk_off(1) + crank * (BM / 2) * 128, 64, head, row,
-                                            b, 0x3, pol_kv);
-                    if (C::N64)
-                        ptx::tma_load_4d_mc(&tmKb, bar, dst + chunk_off(1) + crank * (BM / 2) * 64, 64, head, row, b,
-                                            0x3, pol_kv);
+                    tload(&tmKa, bar, dst + crank * RB * 128, 0, row);
+                    if (C::N128 == 2) tload(&tmKa, bar, dst + chunk_off(1) + crank * RB * 128, 64, row);
+                    if (C::N64) tload(&tmKb, bar, dst + chunk_off(1) + crank * RB * 64, 64, row);
                 }
             }
             __syncwarp();
@@ -284,7 +305,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                 }
                 ptx::mma_commit(&bars->s_full[j % NG]);
-                ptx::mma_commit_mc(&bars->kv_empty[slot], 0x3);
+                if (CL == 1) ptx::mma_commit(&bars->kv_empty[slot]);
+                else ptx::mma_commit_mc(&bars->kv_empty[slot], CL_MASK);
             }
             __syncwarp();
         };
@@ -311,7 +333,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                     (j > 0 || key16 > 0) ? 1u : 0u);
                     }
                     if (hf == 1) {
-                        ptx::mma_commit_mc(&bars->kv_empty[slotV], 0x3);
+                        if (CL == 1) ptx::mma_commit(&bars->kv_empty[slotV]);
+                        else ptx::mma_commit_mc(&bars->kv_empty[slotV], CL_MASK);
                         ptx::mma_commit(&bars->pv_done[t]);
                         if (j == n_kv - 1) ptx::mma_commit(&bars->o_final);
                     }
@@ -360,14 +383,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                 }
 #pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    m0 = fmaxf(m0, __uint_as_float(sa[i]));
-                    m1 = fmaxf(m1, __uint_as_float(sa[i + 1]));
-                    m2 = fmaxf(m2, __uint_as_float(sb[i]));
-                    m3 = fmaxf(m3, __uint_as_float(sb[i + 1]));
+                for (int i = 0; i < 32; i += 4) {   // FMNMX3: two new scores per instruction, four chains
+                    m0 = ptx::fmax3(m0, __uint_as_float(sa[i]), __uint_as_float(sa[i + 1]));
+                    m1 = ptx::fmax3(m1, __uint_as_float(sa[i + 2]), __uint_as_float(sa[i + 3]));
+                    m2 = ptx::fmax3(m2, __uint_as_float(sb[i]), __uint_as_float(sb[i + 1]));
+                    m3 = ptx::fmax3(m3, __uint_as_float(sb[i + 2]), __uint_as_float(sb[i + 3]));
                 }
             }
-            const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl2;
+            const float mx = ptx::fmax3(m0, m1, fmaxf(m2, m3)) * sl2;
             if (tr) TRACE(j, 7);
             // running max after tile j-1, handed over by the previous group (strict tile order)
             float mprev = -INFINITY;
@@ -433,7 +456,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const uint32_t u1 = e + 1 < 32 ? sa[e + 1] : sb[e + 1 - 32];
                     const uint64_t X = ptx::ffma2(ptx::f2pack(__uint_as_float(u0), __uint_as_float(u1)), SL2, NEGM);
                     float p0, p1;
-                    if ((e & 7) >= C::POLY_FROM) {
+                    if ((e & 15) >= C::POLY_FROM) {
                         ex2_poly2(X, p0, p1);
                     } else {
                         float x0, x1;
@@ -461,6 +484,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (tr) TRACE(j, 6);
         }
         // ------------------------------------------------------------ epilogue: merge group sums, O / l -> global
+        ptx::mbar_wait(&bars->o_final, 0);   // ring slot 0 is idle from here on (see xml)
+        ptx::tc_fence_after();
         xml[g][row] = mg;
         xml[NG + g][row] = l;
         ptx::named_bar_sync(BAR_EPI, 32 * NUM_SOFTMAX_WARPS);
@@ -474,8 +499,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (mq != -INFINITY) lsum += xml[NG + q][row] * ptx::ex2(mq - mm);   // a group may have no tile
         }
         const float inv = 1.f / lsum;
-        ptx::mbar_wait(&bars->o_final, 0);
-        ptx::tc_fence_after();
         const long long srow = (long long)qtile * BM + row;
         const bool valid = srow < args.Sq;      // tcgen05.ld is warp-collective: every lane loads, valid lanes store
         uint4 *dst = reinterpret_cast<uint4 *>(args.O + (long long)b * args.o_batch_stride + srow * args.o_tok_stride +
@@ -546,17 +569,17 @@ template <int D>
 cudaError_t launch_d(const AttnProblem &p, cudaStream_t st) {
     using C = Cfg<D>;
     // m[0]/m[1]: Q 64-col SW128 / 32-col SW64 boxes of 128 rows; m[2]/m[3]: the same for K with 64-row boxes
-    // (each CTA of a pair fetches half a tile); m[4]: V 64-col SW128 (D=64/128) or 32-col SW64 (D=96) boxes
+    // (each CTA of a cluster fetches 128/CL rows of a tile); m[4]: V 64-col SW128 (D=64/128) or 32-col SW64 (D=96) boxes
     // of 64 rows; m[5] unused.
     CUtensorMap m[6];
     const int vcols = C::V_SW64 ? 32 : 64;
     bool ok = make_map(&m[0], p.q, D, p.n_heads, p.Sq, p.B, p.q_tok_stride, p.q_batch_stride, 64, false) &&
-              make_map(&m[2], p.k, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, 64, false, BM / 2) &&
+              make_map(&m[2], p.k, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, 64, false, BN / CL) &&
               make_map(&m[4], p.v, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, vcols, C::V_SW64,
-                       BM / 2);
+                       BN / CL);
     if (ok && C::N64)
         ok = make_map(&m[1], p.q, D, p.n_heads, p.Sq, p.B, p.q_tok_stride, p.q_batch_stride, 32, true) &&
-             make_map(&m[3], p.k, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, 32, true, BM / 2);
+             make_map(&m[3], p.k, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, 32, true, BN / CL);
     else {
         m[1] = m[0];
         m[3] = m[2];
@@ -581,13 +604,13 @@ cudaError_t launch_d(const AttnProblem &p, cudaStream_t st) {
     // an odd tile count gets one extra all-out-of-range tile that only helps its partner load.
     const int qtiles = (p.Sq + BM - 1) / BM;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((qtiles + 1) & ~1, p.n_heads, p.B);
+    cfg.gridDim = dim3((qtiles + CL - 1) / CL * CL, p.n_heads, p.B);
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = C::SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;

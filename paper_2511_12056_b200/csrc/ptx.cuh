@@ -191,6 +191,12 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 namespace spa {
 namespace ptx {
 // ------------------------------------------------------------------ packed f32x2 arithmetic (sm_100)
+// three-input max (FMNMX3, sm_100+): halves the instruction count of a row-max reduction
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
 __device__ __forceinline__ uint64_t f2pack(float a, float b) {
     uint64_t r;
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));

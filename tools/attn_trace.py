@@ -4,6 +4,7 @@
     python -m paper_2511_12056_b200._build --trace
     SPA_LIB=paper_2511_12056_b200/lib/libspa_trace.so python tools/attn_trace.py [--D 128]
 Events (clock64 cycles) per KV iteration j of CTA (0,0,0):
+  TMA producer (lane 0):      11 K_j load issued   12 V_j load issued
   MMA issuer (elected lane):  2 K_j acquired -> QK(j) issued   10 V_j acquired
                               0 / 1  P(j) key-half 0 / 1 ready -> PV half issued
   softmax, lane 0 of the lane-quarter-0 warp of group j % NG:
@@ -40,11 +41,11 @@ assert lib.spa_debug_read_trace(ctypes.addressof(buf)) == 0
 T = np.frombuffer(buf, dtype=np.uint64).reshape(256, 16).astype(np.int64)
 n = min(256, (args.S + 127) // 128)
 t0 = T[0, 2]
-print("   j |  QKiss  Vacq   P0rdy   P1rdy |  top    Srdy   max    xchg   P0rel  P1rel")
+print("   j |  Kld    Vld   |  QKiss  Vacq   P0rdy   P1rdy |  top    Srdy   max    xchg   P0rel  P1rel")
 mid0 = n // 2
 for j in list(range(0, args.rows)) + list(range(mid0, mid0 + 6)) + list(range(n - 3, n)):
     r = T[j] - t0
-    print(f"{j:4d} | {r[2]:7d} {r[10]:7d} {r[0]:7d} {r[1]:7d} | {r[3]:7d} {r[4]:7d} {r[7]:7d} {r[5]:7d} {r[8]:7d} {r[6]:7d}")
+    print(f"{j:4d} | {r[11]:7d} {r[12]:7d} | {r[2]:7d} {r[10]:7d} {r[0]:7d} {r[1]:7d} | {r[3]:7d} {r[4]:7d} {r[7]:7d} {r[5]:7d} {r[8]:7d} {r[6]:7d}")
 js = np.arange(n // 4, 3 * n // 4)
 d = T[js]
 ideal = {128: 1024, 96: 768, 64: 512}[args.D]
@@ -54,6 +55,7 @@ print("per tile, mean cycles: "
       f"wait S {np.mean(d[:, 4] - d[:, 3]):.0f} | pass1 {np.mean(d[:, 7] - d[:, 4]):.0f} | "
       f"xchg {np.mean(d[:, 5] - d[:, 7]):.0f} | half0 {np.mean(d[:, 8] - d[:, 5]):.0f} | "
       f"half1 {np.mean(d[:, 6] - d[:, 8]):.0f} | softmax busy {np.mean(d[:, 6] - d[:, 4]):.0f}")
+print(f"TMA latency (issue -> MMA warp sees data): K {np.mean(d[:, 2] - d[:, 11]):.0f}  V {np.mean(d[:, 10] - d[:, 12]):.0f}")
 print("MMA side: "
       f"QK(j) issue -> P0(j) ready {np.mean(d[:, 0] - d[:, 2]):.0f} | P0 -> P1 {np.mean(d[:, 1] - d[:, 0]):.0f} | "
       f"S(j) ready - QK(j) issue {np.mean(d[:, 4] - d[:, 2]):.0f}")
