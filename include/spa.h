@@ -90,11 +90,16 @@ typedef struct {
                        g = h/G_h heads, C = N_st/G_h query chunks; 1 = Ulysses (one stage) */
     int n_src;      /* ranks holding sequence shards: 0 = all ranks (Ulysses/PipeSP);
                        0 < n_src < nranks = Aco (ranks >= n_src are co-processors) */
+    int pad_heads;  /* 0: H % nranks must be 0.  1: head padding ("padding increases
+                       the head count to 28 so that each GPU handles 4 heads"): the heads are padded to
+                       Hp = spa_pad_heads(H, nranks); rank r owns padded heads [r*Hp/nranks, (r+1)*Hp/nranks);
+                       pad heads are never read from q/k/v, never computed and never written to out
+                       (user buffers keep H heads).  DESIGN.md R10. */
 } spa_shape;
 
 /* Validates everything synchronously.  Requirements: D in {64,96,128}; S % n_src == 0;
- * H % nranks == 0 (heads are split over ALL ranks, which own contiguous head blocks);
- * 1 <= stages and C <= S/n_src. */
+ * H % nranks == 0 unless pad_heads (heads are split over ALL ranks, which own contiguous head blocks);
+ * 1 <= stages and C <= S/n_src (C and G_h follow from h = Hp/nranks). */
 spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *shape);
 /* Device workspace bytes the caller must pass as `ws` (per rank; for loopback plans:
  * for all virtual ranks together).  Zero when nranks == 1. */
@@ -112,6 +117,15 @@ spa_status spa_plan_destroy(spa_plan *plan);
  *                          the denoising sub-group instead */
 enum { SPA_OPT_PROFILE = 1, SPA_OPT_SKIP_COMM = 2, SPA_OPT_COPROC_BUSY = 3 };
 spa_status spa_plan_set_option(spa_plan *plan, int option, int value);
+
+/* Key-padding mask for the following SP calls of this plan (Alg. 1's attention_mask, PAPER.md:85 and :90,
+ * which the paper never defines -- DESIGN.md reading R20): kv_len = device int32 [B]; key t of batch entry b
+ * (global sequence position, 0 <= t < S) takes part in the softmax iff t < kv_len[b] (values clamped to
+ * [0, S]); a batch entry with kv_len 0 gives output rows of 0.  Query rows are never masked.  NULL clears
+ * the mask.  The array is read by the kernels when they run (stream-ordered): it must stay valid and
+ * unchanged until the calls' streams complete.  NCCL plans: each rank passes its own device copy.
+ * Masked key tiles are skipped entirely (work scales with kv_len). */
+spa_status spa_plan_set_kv_len(spa_plan *plan, const int32_t *kv_len);
 
 /* Per-step device times (ms) of the last profiled call, once its stream has completed.
  * attn_ms[k], a2a_in_ms[k], a2a_out_ms[k] for k < n_stages (arrays of >= 64 entries). */
@@ -166,6 +180,12 @@ spa_status spa_attention_fwd(const void *q, const void *k, const void *v, void *
                              int n_heads, int D, long long q_tok_stride, long long q_batch_stride,
                              long long kv_tok_stride, long long kv_batch_stride, long long o_tok_stride,
                              long long o_batch_stride, void *stream);
+/* The same with a key-padding mask: kv_len = device int32 [B] (NULL = none); keys t >= kv_len[b]
+ * (clamped to [0, Skv]) take no part; kv_len[b] == 0 gives rows of 0 (R20). */
+spa_status spa_attention_fwd_masked(const void *q, const void *k, const void *v, void *o, int B, int Sq, int Skv,
+                                    int n_heads, int D, long long q_tok_stride, long long q_batch_stride,
+                                    long long kv_tok_stride, long long kv_batch_stride, long long o_tok_stride,
+                                    long long o_batch_stride, const int32_t *kv_len, void *stream);
 
 /* ------------------------------------------------------------------ host-side description (no GPU needed)
  * Buffers: 0 q, 1 k, 2 v, 3 out (the caller's, of source rank `src`), 4 ws (of rank `rank`). */

@@ -142,22 +142,24 @@ struct SmemBars {
 static_assert(sizeof(SmemBars) <= 512, "barrier block");
 
 // Two exp2 at once in f32x2 arithmetic: x = n + f (n = round(x), |f| <= 1/2), 2^f by a degree-3 fit (max rel
-// err 7.5e-5, far below the bf16 rounding of P), 2^n added to the exponent field; x >= -125 keeps it normal.
+// err 7.5e-5, far below the bf16 rounding of P), times 2^n built in the exponent field.  x is clamped to -127,
+// where the scale's exponent field is 0: 2^x < 2^-126.5 (and a masked key's -inf) gives exactly 0, like the
+// flush-to-zero MUFU.EX2 path.
 __device__ __forceinline__ void ex2_poly2(uint64_t X, float &y0, float &y1) {
     float x0, x1;
     ptx::f2unpack(X, x0, x1);
-    const uint64_t Xc = ptx::f2pack(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
+    const uint64_t Xc = ptx::f2pack(fmaxf(x0, -127.f), fmaxf(x1, -127.f));
     const uint64_t T = ptx::fadd2(Xc, ptx::f2pack(12582912.f, 12582912.f));   // 1.5*2^23: low bits = round(x)
     const uint64_t F = ptx::fsub2(Xc, ptx::fadd2(T, ptx::f2pack(-12582912.f, -12582912.f)));
     uint64_t P = ptx::ffma2(ptx::f2pack(0.0551716611f, 0.0551716611f), F, ptx::f2pack(0.242611152f, 0.242611152f));
     P = ptx::ffma2(P, F, ptx::f2pack(0.693260968f, 0.693260968f));
     P = ptx::ffma2(P, F, ptx::f2pack(0.999928057f, 0.999928057f));
-    float p0, p1, t0, t1;
-    ptx::f2unpack(P, p0, p1);
+    float t0, t1;
     ptx::f2unpack(T, t0, t1);
-    // bits(T) = bits(1.5*2^23) + n and bits(1.5*2^23) << 23 == 0 (mod 2^32): one IMAD adds n << 23
-    y0 = __int_as_float(__float_as_int(t0) * (1 << 23) + __float_as_int(p0));
-    y1 = __int_as_float(__float_as_int(t1) * (1 << 23) + __float_as_int(p1));
+    // bits(T) = bits(1.5*2^23) + n and bits(1.5*2^23) << 23 == 0 (mod 2^32): one IMAD gives bits(2^n) = (n+127) << 23
+    const float s0 = __int_as_float(__float_as_int(t0) * (1 << 23) + (127 << 23));
+    const float s1 = __int_as_float(__float_as_int(t1) * (1 << 23) + (127 << 23));
+    ptx::f2unpack(ptx::fmul2(P, ptx::f2pack(s0, s1)), y0, y1);
 }
 
 template <int D>
@@ -182,7 +184,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int qtile = blockIdx.x;
     const int head = blockIdx.y;
     const int b = blockIdx.z;
-    const int n_kv = (args.Skv + BN - 1) / BN;
+    // key-padding mask (Alg. 1 attention_mask; R20): keys t >= kv_len[b] take no
+    // part; tiles wholly beyond it are never loaded.  Both CTAs of a cluster share b, hence n_kv.
+    int Skv_b = args.Skv;
+    if (args.kv_len) {
+        const int L = __ldg(args.kv_len + b);
+        Skv_b = L < 0 ? 0 : (L < Skv_b ? L : Skv_b);
+    }
+    const int n_kv = (Skv_b + BN - 1) / BN;   // 0: every row of this batch entry is 0
 
     if (threadIdx.x == 0) {
         ptx::mbar_init(&bars->q_full, 1);
@@ -219,7 +228,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::setmaxnreg_dec<AUX_REGS>();
         const uint64_t pol_q = ptx::policy_evict_first();
         const uint64_t pol_kv = ptx::policy_evict_last();
-        if (lane == 0) {
+        if (lane == 0 && n_kv > 0) {
             ptx::mbar_arrive_expect_tx(&bars->q_full, C::TILE_BYTES);
             ptx::tma_load_4d(&tmQa, &bars->q_full, sQ, 0, head, qtile * BM, b, pol_q);
             if (C::N128 == 2) ptx::tma_load_4d(&tmQa, &bars->q_full, sQ + chunk_off(1), 64, head, qtile * BM, b, pol_q);
@@ -311,7 +320,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             __syncwarp();
         };
 
-        ptx::mbar_wait(&bars->q_full, 0);
+        if (n_kv > 0) ptx::mbar_wait(&bars->q_full, 0);
         for (int j = 0; j < NG && j < n_kv; ++j) issue_qk(j);
         for (int j = 0; j < n_kv; ++j) {
             const int t = j % NG;
@@ -354,7 +363,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t tO = tmem + lane_base + C::O_COL;
         const float sl2 = args.scale_log2;
         const uint64_t SL2 = ptx::f2pack(sl2, sl2);
-        const int last_valid = args.Skv - (n_kv - 1) * BN;   // valid keys in the last tile (1..128)
+        const int last_valid = Skv_b - (n_kv - 1) * BN;   // valid keys in the last tile (1..128)
         const bool tr = (lane == 0 && wq == 0);
         const uint32_t bar_in = 1 + 3 * wq + g;                  // "m of tile j-1 is in xm[]" for this warp
         const uint32_t bar_out = 1 + 3 * wq + (g + 1) % NG;      // ... for the warp of the next group
@@ -484,8 +493,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (tr) TRACE(j, 6);
         }
         // ------------------------------------------------------------ epilogue: merge group sums, O / l -> global
-        ptx::mbar_wait(&bars->o_final, 0);   // ring slot 0 is idle from here on (see xml)
-        ptx::tc_fence_after();
+        if (n_kv > 0) {
+            ptx::mbar_wait(&bars->o_final, 0);   // ring slot 0 is idle from here on (see xml)
+            ptx::tc_fence_after();
+        }
         xml[g][row] = mg;
         xml[NG + g][row] = l;
         ptx::named_bar_sync(BAR_EPI, 32 * NUM_SOFTMAX_WARPS);
@@ -498,7 +509,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const float mq = xml[q][row];
             if (mq != -INFINITY) lsum += xml[NG + q][row] * ptx::ex2(mq - mm);   // a group may have no tile
         }
-        const float inv = 1.f / lsum;
+        const float inv = n_kv > 0 ? 1.f / lsum : 0.f;   // no valid key: the row is 0 (R20)
         const long long srow = (long long)qtile * BM + row;
         const bool valid = srow < args.Sq;      // tcgen05.ld is warp-collective: every lane loads, valid lanes store
         uint4 *dst = reinterpret_cast<uint4 *>(args.O + (long long)b * args.o_batch_stride + srow * args.o_tok_stride +
@@ -509,8 +520,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (c % NG != g) continue;
             const int col = 16 * c;
             uint32_t r[16];
-            ptx::tmem_ld16(tO + col, r);
-            ptx::tmem_wait_ld();
+            if (n_kv > 0) {
+                ptx::tmem_ld16(tO + col, r);
+                ptx::tmem_wait_ld();
+            } else {
+#pragma unroll
+                for (int u = 0; u < 16; ++u) r[u] = 0u;
+            }
             uint32_t w[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u)
@@ -600,6 +616,7 @@ cudaError_t launch_d(const AttnProblem &p, cudaStream_t st) {
     a.Sq = p.Sq;
     a.Skv = p.Skv;
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+    a.kv_len = p.kv_len;
     // clusters of 2 CTAs (adjacent query tiles of one head) share every K/V tile via TMA multicast;
     // an odd tile count gets one extra all-out-of-range tile that only helps its partner load.
     const int qtiles = (p.Sq + BM - 1) / BM;

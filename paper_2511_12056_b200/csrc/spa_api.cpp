@@ -89,6 +89,8 @@ struct spa_plan {
     int P = 1;      // ranks owning heads (all ranks)
     int Psrc = 1;   // ranks holding sequence shards
     int h = 1, S_l = 1;
+    int Hp = 1;     // heads after padding to a multiple of P (== sh.H unless shape.pad_heads)
+    const int32_t *kv_len = nullptr;   // key-padding lengths, device int32 [B] (spa_plan_set_kv_len) or NULL
     Split split;
     // per-rank workspace layout (bytes)
     long long E_src = 0, E_own = 0;  // elements of one send-side / owner-side tensor
@@ -188,27 +190,61 @@ void gen_out_msgs(const spa_plan *p, const Split &s, int k, int r, int o_send_bu
     }
 }
 
-// Pack (source rank): send[kh][q][b][t][jj][d] = X[b][t][q*h + kh*g + jj][d]
-CopyJob pack_job(const spa_plan *p, const Split &s, const void *x, long long dst_off, uint8_t *ws) {
+// Real (unpadded) heads of head group kh owned by rank q: global heads q*h + kh*g + jj < H.
+int real_heads(const spa_plan *p, const Split &s, int q, int kh) {
+    return std::max(0, std::min(s.g, p->sh.H - (q * p->h + kh * s.g)));
+}
+
+// Pack (source rank): send[kh][q][b][t][jj][d] = X[b][t][q*h + kh*g + jj][d].
+// One 4-level job when every head group is complete; with padded heads one job per (kh, q) that copies only
+// the real heads of the group (pad-head slots of the send buffer are never written nor read as results).
+void pack_jobs(const spa_plan *p, const Split &s, const void *x, long long dst_off, uint8_t *ws,
+               std::vector<CopyJob> &out) {
     const long long D2 = (long long)p->sh.D * 2, H = p->sh.H;
-    CopyJob j{};
-    j.src = reinterpret_cast<const uint8_t *>(x);
-    j.dst = ws + dst_off;
-    j.count[0] = s.G_h; j.count[1] = p->P; j.count[2] = p->sh.B; j.count[3] = p->S_l;
-    j.src_stride[0] = s.g * D2; j.src_stride[1] = p->h * D2; j.src_stride[2] = p->S_l * H * D2; j.src_stride[3] = H * D2;
     const long long run = s.g * D2;
-    j.dst_stride[3] = run; j.dst_stride[2] = p->S_l * run; j.dst_stride[1] = p->sh.B * p->S_l * run;
-    j.dst_stride[0] = p->P * p->sh.B * p->S_l * run;
-    j.run_bytes = run;
-    return j;
+    // x == NULL / ws == NULL (describe): the job pointers hold plain byte offsets
+    const uintptr_t xb = reinterpret_cast<uintptr_t>(x);
+    const uintptr_t wb = ws ? reinterpret_cast<uintptr_t>(ws) + (uintptr_t)dst_off : 0;
+    auto at = [](uintptr_t base, long long off) { return reinterpret_cast<uint8_t *>(base + (uintptr_t)off); };
+    if (p->Hp == p->sh.H) {
+        CopyJob j{};
+        j.src = at(xb, 0);
+        j.dst = at(wb, 0);
+        j.count[0] = s.G_h; j.count[1] = p->P; j.count[2] = p->sh.B; j.count[3] = p->S_l;
+        j.src_stride[0] = s.g * D2; j.src_stride[1] = p->h * D2; j.src_stride[2] = p->S_l * H * D2;
+        j.src_stride[3] = H * D2;
+        j.dst_stride[3] = run; j.dst_stride[2] = p->S_l * run; j.dst_stride[1] = p->sh.B * p->S_l * run;
+        j.dst_stride[0] = p->P * p->sh.B * p->S_l * run;
+        j.run_bytes = run;
+        out.push_back(j);
+        return;
+    }
+    for (int kh = 0; kh < s.G_h; ++kh)
+        for (int q = 0; q < p->P; ++q) {
+            const int nreal = real_heads(p, s, q, kh);
+            if (nreal == 0) continue;
+            CopyJob j{};
+            j.src = at(xb, (q * p->h + kh * s.g) * D2);
+            j.dst = at(wb, idx_send(p, s, kh, q, 0, 0) * 2);
+            j.count[0] = 1; j.count[1] = 1; j.count[2] = p->sh.B; j.count[3] = p->S_l;
+            j.src_stride[2] = p->S_l * H * D2; j.src_stride[3] = H * D2;
+            j.dst_stride[2] = p->S_l * run; j.dst_stride[3] = run;
+            j.run_bytes = nreal * D2;
+            out.push_back(j);
+        }
 }
 // Unpack (source rank), Psi_g fused: out[b][t][q*h + kh*g + jj][d] = orecv[kh][q][b][t][jj][d]  (a5)
-CopyJob unpack_job(const spa_plan *p, const Split &s, uint8_t *ws, long long src_off, void *out) {
-    CopyJob j = pack_job(p, s, nullptr, 0, nullptr);
-    std::swap(j.src_stride, j.dst_stride);
-    j.src = ws + src_off;
-    j.dst = reinterpret_cast<uint8_t *>(out);
-    return j;
+void unpack_jobs(const spa_plan *p, const Split &s, uint8_t *ws, long long src_off, void *outp,
+                 std::vector<CopyJob> &out) {
+    const size_t first = out.size();
+    pack_jobs(p, s, nullptr, 0, nullptr, out);
+    for (size_t i = first; i < out.size(); ++i) {
+        CopyJob &j = out[i];
+        std::swap(j.src_stride, j.dst_stride);
+        const uintptr_t src_rel = reinterpret_cast<uintptr_t>(j.dst), dst_rel = reinterpret_cast<uintptr_t>(j.src);
+        j.src = reinterpret_cast<const uint8_t *>((ws ? reinterpret_cast<uintptr_t>(ws) + (uintptr_t)src_off : 0) + src_rel);
+        j.dst = reinterpret_cast<uint8_t *>(reinterpret_cast<uintptr_t>(outp) + dst_rel);
+    }
 }
 
 spa_copy_desc to_desc(const CopyJob &j, int sb, int sr, long long so, int db, int dr, long long dof) {
@@ -340,13 +376,16 @@ spa_status run_attention(Exec &x, int k, cudaStream_t st) {
     const int nr = (p->comm->kind == KIND_LOOPBACK) ? p->P : 1;
     for (int rr = 0; rr < nr; ++rr) {
         const int r = (p->comm->kind == KIND_LOOPBACK) ? rr : p->comm->rank;
+        const int nreal = real_heads(p, s, r, kh);   // pad heads are not computed
+        if (nreal == 0) continue;
         uint8_t *ws = resolve(x, r, BUF_WS, 0);
         AttnProblem a{};
         a.q = ws + p->off_recvQ + base_stage(p, s, kh, c) * 2;
         a.k = ws + p->off_recvK + idx_kv(p, s, kh, 0, 0) * 2;
         a.v = ws + p->off_recvV + idx_kv(p, s, kh, 0, 0) * 2;
         a.o = ws + p->off_O + base_stage(p, s, kh, c) * 2;
-        a.B = p->sh.B; a.Sq = (int)(p->Psrc * L); a.Skv = p->sh.S; a.n_heads = s.g; a.D = p->sh.D;
+        a.B = p->sh.B; a.Sq = (int)(p->Psrc * L); a.Skv = p->sh.S; a.n_heads = nreal; a.D = p->sh.D;
+        a.kv_len = p->kv_len;
         a.q_tok_stride = a.kv_tok_stride = a.o_tok_stride = (long long)s.g * p->sh.D;
         a.q_batch_stride = a.o_batch_stride = p->Psrc * L * s.g * p->sh.D;
         a.kv_batch_stride = (long long)p->sh.S * s.g * p->sh.D;
@@ -363,9 +402,9 @@ spa_status run_pack(Exec &x) {
     for (int i = 0; i < nr; ++i) {
         const int r = (p->comm->kind == KIND_LOOPBACK) ? i : p->comm->rank;
         uint8_t *ws = resolve(x, r, BUF_WS, 0);
-        if (x.in_tensors & 1) jobs.push_back(pack_job(p, *x.s, x.ptr.q[i], p->off_sendQ, ws));
-        if (x.in_tensors & 2) jobs.push_back(pack_job(p, *x.s, x.ptr.k[i], p->off_sendK, ws));
-        if (x.in_tensors & 4) jobs.push_back(pack_job(p, *x.s, x.ptr.v[i], p->off_sendV, ws));
+        if (x.in_tensors & 1) pack_jobs(p, *x.s, x.ptr.q[i], p->off_sendQ, ws, jobs);
+        if (x.in_tensors & 2) pack_jobs(p, *x.s, x.ptr.k[i], p->off_sendK, ws, jobs);
+        if (x.in_tensors & 4) pack_jobs(p, *x.s, x.ptr.v[i], p->off_sendV, ws, jobs);
     }
     if (jobs.empty()) return SPA_OK;
     SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sc, &p->copy_launches));
@@ -378,7 +417,7 @@ spa_status run_unpack(Exec &x) {
     const int nr = (p->comm->kind == KIND_LOOPBACK) ? p->Psrc : (is_source(p, p->comm->rank) ? 1 : 0);
     for (int i = 0; i < nr; ++i) {
         const int r = (p->comm->kind == KIND_LOOPBACK) ? i : p->comm->rank;
-        jobs.push_back(unpack_job(p, *x.s, resolve(x, r, BUF_WS, 0), p->off_orecv, x.ptr.out[i]));
+        unpack_jobs(p, *x.s, resolve(x, r, BUF_WS, 0), p->off_orecv, x.ptr.out[i], jobs);
     }
     if (jobs.empty()) return SPA_OK;
     SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sc, &p->copy_launches));
@@ -418,6 +457,7 @@ spa_status execute(Exec &x) {
             AttnProblem a{};
             a.q = x.ptr.q[0]; a.k = x.ptr.k[0]; a.v = x.ptr.v[0]; a.o = x.ptr.out[0];
             a.B = p->sh.B; a.Sq = a.Skv = p->sh.S; a.n_heads = p->sh.H; a.D = p->sh.D;
+            a.kv_len = p->kv_len;
             a.q_tok_stride = a.kv_tok_stride = a.o_tok_stride = (long long)p->sh.H * p->sh.D;
             a.q_batch_stride = a.kv_batch_stride = a.o_batch_stride = (long long)p->sh.S * p->sh.H * p->sh.D;
             pr.begin("attn0", x.sc);
@@ -673,16 +713,19 @@ spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *sha
     const int Psrc = s.n_src == 0 ? P : s.n_src;
     if (Psrc < 1 || Psrc > P) return fail(SPA_ERR_SHAPE, "n_src must be in [0, nranks]");
     if (s.S % Psrc) return fail(SPA_ERR_SHAPE, "S must be divisible by the number of source ranks");
-    if (s.H % P) return fail(SPA_ERR_SHAPE, "H must be divisible by nranks (pad heads first: spa_pad_heads)");
+    if (s.pad_heads != 0 && s.pad_heads != 1) return fail(SPA_ERR_INVALID, "pad_heads must be 0 or 1");
+    if (s.H % P && !s.pad_heads)
+        return fail(SPA_ERR_SHAPE, "H must be divisible by nranks (or set shape.pad_heads = 1)");
     spa_plan *p = new spa_plan;
     p->comm = comm; p->sh = s; p->P = P; p->Psrc = Psrc;
-    p->h = s.H / P; p->S_l = s.S / Psrc;
+    p->Hp = (s.H + P - 1) / P * P;
+    p->h = p->Hp / P; p->S_l = s.S / Psrc;
     p->split = make_split(p->h, p->S_l, s.stages);
     if (p->split.C > p->S_l) {
         delete p;
         return fail(SPA_ERR_SHAPE, "more query chunks than local tokens");
     }
-    p->E_src = (long long)s.B * p->S_l * s.H * s.D;
+    p->E_src = (long long)s.B * p->S_l * p->Hp * s.D;   // send / orecv: all (padded) head groups
     p->E_own = (long long)s.B * s.S * p->h * s.D;
     if (P > 1) {
         long long off = 0;
@@ -729,6 +772,13 @@ spa_status spa_plan_set_option(spa_plan *plan, int option, int value) {
         case SPA_OPT_COPROC_BUSY: plan->coproc_busy = value != 0; break;
         default: return fail(SPA_ERR_INVALID, "unknown option");
     }
+    return SPA_OK;
+}
+
+spa_status spa_plan_set_kv_len(spa_plan *plan, const int32_t *kv_len) {
+    if (!plan) return fail(SPA_ERR_INVALID, "plan is NULL");
+    if (kv_len && reinterpret_cast<uintptr_t>(kv_len) % 4) return fail(SPA_ERR_INVALID, "kv_len not 4-byte aligned");
+    plan->kv_len = kv_len;
     return SPA_OK;
 }
 
@@ -852,10 +902,10 @@ spa_status spa_reshard_head_to_seq_local(spa_plan *plan, const void *const x_hea
     return reshard_call(plan, plan->P, xx.data(), xh.data(), ws, stream, true, false);
 }
 
-spa_status spa_attention_fwd(const void *q, const void *k, const void *v, void *o, int B, int Sq, int Skv,
-                             int n_heads, int D, long long q_tok_stride, long long q_batch_stride,
-                             long long kv_tok_stride, long long kv_batch_stride, long long o_tok_stride,
-                             long long o_batch_stride, void *stream) {
+spa_status spa_attention_fwd_masked(const void *q, const void *k, const void *v, void *o, int B, int Sq, int Skv,
+                                    int n_heads, int D, long long q_tok_stride, long long q_batch_stride,
+                                    long long kv_tok_stride, long long kv_batch_stride, long long o_tok_stride,
+                                    long long o_batch_stride, const int32_t *kv_len, void *stream) {
     SPA_TRY(check_ptr(q, "q")); SPA_TRY(check_ptr(k, "k")); SPA_TRY(check_ptr(v, "v")); SPA_TRY(check_ptr(o, "o"));
     if (D != 64 && D != 96 && D != 128) return fail(SPA_ERR_UNSUPPORTED, "D must be 64, 96 or 128");
     if (B < 1 || Sq < 1 || Skv < 1 || n_heads < 1) return fail(SPA_ERR_SHAPE, "B, Sq, Skv, n_heads must be >= 1");
@@ -864,11 +914,20 @@ spa_status spa_attention_fwd(const void *q, const void *k, const void *v, void *
     if (q_tok_stride < (long long)n_heads * D || kv_tok_stride < (long long)n_heads * D ||
         o_tok_stride < (long long)n_heads * D)
         return fail(SPA_ERR_SHAPE, "token stride smaller than n_heads*D");
+    if (kv_len && reinterpret_cast<uintptr_t>(kv_len) % 4) return fail(SPA_ERR_INVALID, "kv_len not 4-byte aligned");
     AttnProblem a{q, k, v, o, B, Sq, Skv, n_heads, D, q_tok_stride, q_batch_stride,
-                  kv_tok_stride, kv_batch_stride, o_tok_stride, o_batch_stride};
+                  kv_tok_stride, kv_batch_stride, o_tok_stride, o_batch_stride, kv_len};
     cudaError_t e = launch_attention(a, reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return fail(SPA_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
     return SPA_OK;
+}
+
+spa_status spa_attention_fwd(const void *q, const void *k, const void *v, void *o, int B, int Sq, int Skv,
+                             int n_heads, int D, long long q_tok_stride, long long q_batch_stride,
+                             long long kv_tok_stride, long long kv_batch_stride, long long o_tok_stride,
+                             long long o_batch_stride, void *stream) {
+    return spa_attention_fwd_masked(q, k, v, o, B, Sq, Skv, n_heads, D, q_tok_stride, q_batch_stride, kv_tok_stride,
+                                    kv_batch_stride, o_tok_stride, o_batch_stride, nullptr, stream);
 }
 
 // ------------------------------------------------------------------ describe (host only)
@@ -876,12 +935,16 @@ spa_status spa_plan_describe_pack(const spa_plan *plan, int rank, spa_copy_desc 
     if (!plan || !n) return fail(SPA_ERR_INVALID, "NULL argument");
     *n = 0;
     if (plan->P == 1 || !is_source(plan, rank)) return SPA_OK;
-    const Split &s = plan->split;
     const long long offs[3] = {plan->off_sendQ, plan->off_sendK, plan->off_sendV};
     for (int t = 0; t < 3; ++t) {
-        if (*n >= max) return fail(SPA_ERR_INVALID, "describe: output too small");
-        CopyJob j = pack_job(plan, s, nullptr, 0, nullptr);
-        out[(*n)++] = to_desc(j, BUF_Q + t, rank, 0, BUF_WS, rank, offs[t]);
+        std::vector<CopyJob> jobs;
+        pack_jobs(plan, plan->split, nullptr, 0, nullptr, jobs);
+        for (const CopyJob &j : jobs) {
+            if (*n >= max) return fail(SPA_ERR_INVALID, "describe: output too small");
+            // job pointers are offsets from NULL here: source offset into the user buffer, destination into ws
+            out[(*n)++] = to_desc(j, BUF_Q + t, rank, (long long)reinterpret_cast<uintptr_t>(j.src), BUF_WS, rank,
+                                  offs[t] + (long long)reinterpret_cast<uintptr_t>(j.dst));
+        }
     }
     return SPA_OK;
 }
@@ -890,9 +953,13 @@ spa_status spa_plan_describe_unpack(const spa_plan *plan, int rank, spa_copy_des
     if (!plan || !n) return fail(SPA_ERR_INVALID, "NULL argument");
     *n = 0;
     if (plan->P == 1 || !is_source(plan, rank)) return SPA_OK;
-    if (max < 1) return fail(SPA_ERR_INVALID, "describe: output too small");
-    CopyJob j = unpack_job(plan, plan->split, nullptr, 0, nullptr);
-    out[(*n)++] = to_desc(j, BUF_WS, rank, plan->off_orecv, BUF_OUT, rank, 0);
+    std::vector<CopyJob> jobs;
+    unpack_jobs(plan, plan->split, nullptr, 0, nullptr, jobs);
+    for (const CopyJob &j : jobs) {
+        if (*n >= max) return fail(SPA_ERR_INVALID, "describe: output too small");
+        out[(*n)++] = to_desc(j, BUF_WS, rank, plan->off_orecv + (long long)reinterpret_cast<uintptr_t>(j.src),
+                              BUF_OUT, rank, (long long)reinterpret_cast<uintptr_t>(j.dst));
+    }
     return SPA_OK;
 }
 
@@ -922,7 +989,7 @@ spa_status spa_plan_describe_attention(const spa_plan *p, int stage, int rank, s
     out->k_off = p->off_recvK + idx_kv(p, s, kh, 0, 0) * 2;
     out->v_off = p->off_recvV + idx_kv(p, s, kh, 0, 0) * 2;
     out->o_off = p->off_O + base_stage(p, s, kh, c) * 2;
-    out->B = p->sh.B; out->Sq = (int)(p->Psrc * L); out->Skv = p->sh.S; out->n_heads = s.g;
+    out->B = p->sh.B; out->Sq = (int)(p->Psrc * L); out->Skv = p->sh.S; out->n_heads = real_heads(p, s, rank, kh);
     out->q_tok_stride = out->kv_tok_stride = (long long)s.g * p->sh.D;
     out->q_batch_stride = p->Psrc * L * s.g * p->sh.D;
     out->kv_batch_stride = (long long)p->sh.S * s.g * p->sh.D;

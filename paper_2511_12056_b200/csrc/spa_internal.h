@@ -16,6 +16,7 @@ struct AttnProblem {
     long long q_tok_stride, q_batch_stride;
     long long kv_tok_stride, kv_batch_stride;
     long long o_tok_stride, o_batch_stride;
+    const int32_t *kv_len = nullptr;   // key padding: device int32 [B], keys t >= kv_len[b] masked (NULL: none)
 };
 
 // Kernel-side arguments (tensor maps travel separately as __grid_constant__ parameters).
@@ -24,6 +25,7 @@ struct AttnArgs {
     long long o_tok_stride, o_batch_stride;
     int Sq, Skv;
     float scale_log2;
+    const int32_t *kv_len;   // NULL or device [B]
 };
 
 cudaError_t launch_attention(const AttnProblem &p, cudaStream_t st);

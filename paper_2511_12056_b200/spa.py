@@ -15,7 +15,7 @@ from . import _build
 
 __all__ = [
     "SpaError", "load", "header_functions", "get_unique_id", "Comm", "Plan", "Shape", "Profile",
-    "spa_attention_fwd", "spa_pipesp_attention", "spa_ulysses_attention", "spa_aco_attention",
+    "spa_attention_fwd", "spa_attention_fwd_masked", "spa_pipesp_attention", "spa_ulysses_attention", "spa_aco_attention",
     "spa_pipesp_attention_local", "spa_ulysses_attention_local", "spa_aco_attention_local",
     "spa_reshard_seq_to_head", "spa_reshard_head_to_seq", "spa_reshard_seq_to_head_local",
     "spa_reshard_head_to_seq_local", "spa_pad_heads", "attention", "BUF_Q", "BUF_K", "BUF_V", "BUF_OUT",
@@ -35,7 +35,7 @@ class SpaError(RuntimeError):
 
 class Shape(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int), ("S", ctypes.c_int), ("H", ctypes.c_int), ("D", ctypes.c_int),
-                ("stages", ctypes.c_int), ("n_src", ctypes.c_int)]
+                ("stages", ctypes.c_int), ("n_src", ctypes.c_int), ("pad_heads", ctypes.c_int)]
 
 
 class Profile(ctypes.Structure):
@@ -101,6 +101,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "spa_plan_stage_split": ([_P, ip, ip, ip], i),
         "spa_plan_destroy": ([_P], i),
         "spa_plan_set_option": ([_P, i, i], i),
+        "spa_plan_set_kv_len": ([_P, _P], i),
         "spa_plan_last_profile": ([_P, ctypes.POINTER(Profile)], i),
         "spa_ulysses_attention": ([_P, _P, _P, _P, _P, _P, _P], i),
         "spa_pipesp_attention": ([_P, _P, _P, _P, _P, _P, _P], i),
@@ -113,6 +114,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "spa_reshard_seq_to_head_local": ([_P, _PP, _PP, _P, _P], i),
         "spa_reshard_head_to_seq_local": ([_P, _PP, _PP, _P, _P], i),
         "spa_attention_fwd": ([_P, _P, _P, _P, i, i, i, i, i, _LL, _LL, _LL, _LL, _LL, _LL, _P], i),
+        "spa_attention_fwd_masked": ([_P, _P, _P, _P, i, i, i, i, i, _LL, _LL, _LL, _LL, _LL, _LL, _P, _P], i),
         "spa_plan_describe_pack": ([_P, i, ctypes.POINTER(CopyDesc), i, ip], i),
         "spa_plan_describe_unpack": ([_P, i, ctypes.POINTER(CopyDesc), i, ip], i),
         "spa_plan_describe_messages": ([_P, i, i, i, ctypes.POINTER(Msg), i, ip], i),
@@ -221,9 +223,10 @@ class Comm:
 
 
 class Plan:
-    def __init__(self, comm: Comm, B: int, S: int, H: int, D: int, stages: int = 1, n_src: int = 0):
+    def __init__(self, comm: Comm, B: int, S: int, H: int, D: int, stages: int = 1, n_src: int = 0,
+                 pad_heads: bool = False):
         self.comm = comm
-        self.shape = Shape(B, S, H, D, stages, n_src)
+        self.shape = Shape(B, S, H, D, stages, n_src, int(bool(pad_heads)))
         h = ctypes.c_void_p()
         _check(load().spa_plan_create(ctypes.byref(h), comm.h, ctypes.byref(self.shape)), "spa_plan_create")
         self.h = h
@@ -246,6 +249,11 @@ class Plan:
     def set_option(self, option: int, value: int):
         _check(load().spa_plan_set_option(self.h, option, value), "spa_plan_set_option")
 
+    def set_kv_len(self, kv_len):
+        """Key-padding lengths (device int32 tensor [B], kept alive by the caller) or None."""
+        self._kv_len = kv_len   # keep the tensor referenced while the plan may read it
+        _check(load().spa_plan_set_kv_len(self.h, _ptr(kv_len)), "spa_plan_set_kv_len")
+
     def last_profile(self) -> Profile:
         p = Profile()
         _check(load().spa_plan_last_profile(self.h, ctypes.byref(p)), "spa_plan_last_profile")
@@ -257,15 +265,17 @@ class Plan:
 
     # -- host-side descriptions (no GPU needed)
     def describe_pack(self, rank: int) -> List[CopyDesc]:
-        out = (CopyDesc * 16)()
+        cap = 3 * self.comm.nranks * max(1, self.H) + 16
+        out = (CopyDesc * cap)()
         n = ctypes.c_int()
-        _check(load().spa_plan_describe_pack(self.h, rank, out, 16, ctypes.byref(n)), "describe_pack")
+        _check(load().spa_plan_describe_pack(self.h, rank, out, cap, ctypes.byref(n)), "describe_pack")
         return list(out[:n.value])
 
     def describe_unpack(self, rank: int) -> List[CopyDesc]:
-        out = (CopyDesc * 16)()
+        cap = self.comm.nranks * max(1, self.H) + 16
+        out = (CopyDesc * cap)()
         n = ctypes.c_int()
-        _check(load().spa_plan_describe_unpack(self.h, rank, out, 16, ctypes.byref(n)), "describe_unpack")
+        _check(load().spa_plan_describe_unpack(self.h, rank, out, cap, ctypes.byref(n)), "describe_unpack")
         return list(out[:n.value])
 
     def describe_messages(self, stage: int, direction: int, rank: int) -> List[Msg]:
@@ -295,16 +305,30 @@ def spa_attention_fwd(q, k, v, o, B, Sq, Skv, n_heads, D, q_tok_stride, q_batch_
                                     _stream(stream)), "spa_attention_fwd")
 
 
-def attention(q, k, v, out=None, stream=None):
-    """Single-GPU multi-head attention on contiguous bf16 [B, S, H, D] tensors (all heads)."""
+def spa_attention_fwd_masked(q, k, v, o, B, Sq, Skv, n_heads, D, q_tok_stride, q_batch_stride, kv_tok_stride,
+                             kv_batch_stride, o_tok_stride, o_batch_stride, kv_len, stream=None):
+    _check(load().spa_attention_fwd_masked(_ptr(q), _ptr(k), _ptr(v), _ptr(o), B, Sq, Skv, n_heads, D,
+                                           q_tok_stride, q_batch_stride, kv_tok_stride, kv_batch_stride,
+                                           o_tok_stride, o_batch_stride, _ptr(kv_len), _stream(stream)),
+           "spa_attention_fwd_masked")
+
+
+def attention(q, k, v, out=None, stream=None, kv_len=None):
+    """Single-GPU multi-head attention on contiguous bf16 [B, S, H, D] tensors (all heads).
+    kv_len: optional device int32 [B] key-padding lengths (keys t >= kv_len[b] masked)."""
     import torch
     assert q.dtype == torch.bfloat16 and q.is_contiguous() and k.is_contiguous() and v.is_contiguous()
     B, Sq, H, D = q.shape
     Skv = k.shape[1]
     if out is None:
         out = torch.empty_like(q)
-    spa_attention_fwd(q, k, v, out, B, Sq, Skv, H, D, H * D, Sq * H * D, H * D, Skv * H * D, H * D, Sq * H * D,
-                      stream)
+    if kv_len is None:
+        spa_attention_fwd(q, k, v, out, B, Sq, Skv, H, D, H * D, Sq * H * D, H * D, Skv * H * D, H * D,
+                          Sq * H * D, stream)
+    else:
+        assert kv_len.dtype == torch.int32 and kv_len.is_cuda and kv_len.numel() == B
+        spa_attention_fwd_masked(q, k, v, out, B, Sq, Skv, H, D, H * D, Sq * H * D, H * D, Skv * H * D, H * D,
+                                 Sq * H * D, kv_len, stream)
     return out
 
 

@@ -44,10 +44,10 @@ def exchange(plans, stage: int, direction: int, ws):
 def identity_attention(plan, stage: int, rank: int, wsr: np.ndarray):
     """O := Q for the stage's query rows (checks the attention descriptor's Q/O regions)."""
     a = plan.describe_attention(stage, rank)
-    n = a.B * a.Sq * a.n_heads * plan.D * 2
+    n = a.B * a.Sq * a.q_tok_stride * 2   # whole token rows of the group (pad-head slots included)
     wsr[a.o_off:a.o_off + n] = wsr[a.q_off:a.q_off + n]
     # K/V regions must hold full sequences of the stage's heads: touch-check the extents
-    kv = a.B * a.Skv * a.n_heads * plan.D * 2
+    kv = a.B * a.Skv * a.kv_tok_stride * 2
     assert a.k_off + kv <= len(wsr) and a.v_off + kv <= len(wsr)
 
 

@@ -42,6 +42,39 @@ def test_plan_validation(shape, err):
     assert e.value.status == err
 
 
+def test_pad_heads_flag_accepts_indivisible_heads():
+    comm = spa.Comm.host(7, 0)
+    with pytest.raises(spa.SpaError) as e:
+        spa.Plan(comm, 1, 7 * 16, 24, 64)
+    assert e.value.status == 2
+    p = spa.Plan(comm, 1, 7 * 16, 24, 64, pad_heads=True)   # 24 heads on 7 GPUs -> 28
+    assert p.stage_split == (1, 1, 4)
+    # rank 6 owns padded heads 24..27 only: nothing to compute there
+    assert spa.Plan(spa.Comm.host(7, 6), 1, 7 * 16, 24, 64, pad_heads=True).describe_attention(0, 6).n_heads == 0
+    assert p.describe_attention(0, 5).n_heads == 4
+
+
+@pytest.mark.parametrize("P,H,S,B,stages", [
+    (4, 6, 32, 1, 1), (4, 6, 32, 2, 2), (3, 4, 36, 1, 2), (7, 24, 7 * 6, 1, 1), (7, 24, 7 * 6, 1, 4),
+    (8, 20, 64, 1, 3), (2, 3, 16, 1, 2),
+])
+def test_host_path_padded_heads(P, H, S, B, stages):
+    """Head padding: only real heads are packed, computed and unpacked."""
+    D = 64
+    plans = [spa.Plan(spa.Comm.host(P, r), B, S, H, D, stages=stages, pad_heads=True) for r in range(P)]
+    xs, _ = _labels(B, S, H, D, P)
+    outs = hostsim.run_path(plans, xs, xs, xs)
+    for r in range(P):
+        assert np.array_equal(outs[r], xs[r]), r
+    Hp = -(-H // P) * P
+    h = Hp // P
+    G_h, C, g = plans[0].stage_split
+    for r in range(P):
+        for k in range(G_h * C):
+            kh = k // C
+            assert plans[r].describe_attention(k, r).n_heads == max(0, min(g, H - (r * h + kh * g)))
+
+
 def test_host_comm_cannot_execute():
     comm = spa.Comm.host(2, 1)
     plan = spa.Plan(comm, 1, 256, 4, 64, stages=2)
