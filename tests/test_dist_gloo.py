@@ -4,7 +4,8 @@ Each process plays one rank: it builds the plan on a host-only comm (same plan a
 runs the described pack jobs, exchanges exactly the described per-stage messages with the other
 process through torch.distributed (gloo) point-to-point, applies an identity "attention" to the
 described regions, runs the output exchange and the described unpack (Psi_g).  The output must
-equal the input element for element, for every stage split and for Aco (1 source + 1 co-processor).
+equal the input element for element, for every stage split, for Aco (1 source + 1 co-processor) and
+for head padding (H odd).
 """
 import os
 import socket
@@ -61,8 +62,8 @@ def _worker(rank, world, port, cases, result):
     from paper_2511_12056_b200 import spa
     from tests import hostsim
     ok = True
-    for (B, S, H, D, stages, n_src) in cases:
-        plan = spa.Plan(spa.Comm.host(world, rank), B, S, H, D, stages=stages, n_src=n_src)
+    for (B, S, H, D, stages, n_src, pad) in cases:
+        plan = spa.Plan(spa.Comm.host(world, rank), B, S, H, D, stages=stages, n_src=n_src, pad_heads=pad)
         nsrc = n_src or world
         S_l = S // nsrc
         X = ((np.arange(B * S * H * D) * 2654435761) % 65521).astype(np.uint16).reshape(B, S, H, D)
@@ -89,8 +90,10 @@ def _worker(rank, world, port, cases, result):
 
 @pytest.mark.timeout(300)
 def test_two_process_gloo_exchange():
-    cases = [(1, 64, 4, 64, 1, 0), (1, 64, 4, 64, 2, 0), (2, 64, 4, 96, 4, 0), (1, 128, 8, 128, 8, 0),
-             (1, 96, 6, 64, 6, 0), (1, 48, 2, 64, 1, 1), (2, 48, 4, 64, 2, 1)]
+    # (B, S, H, D, stages, n_src, pad_heads); the last two: H odd over 2 ranks with head padding
+    cases = [(1, 64, 4, 64, 1, 0, 0), (1, 64, 4, 64, 2, 0, 0), (2, 64, 4, 96, 4, 0, 0), (1, 128, 8, 128, 8, 0, 0),
+             (1, 96, 6, 64, 6, 0, 0), (1, 48, 2, 64, 1, 1, 0), (2, 48, 4, 64, 2, 1, 0), (1, 64, 3, 64, 2, 0, 1),
+             (2, 64, 5, 96, 3, 0, 1)]
     world = 2
     ctx = mp.get_context("spawn")
     result = ctx.Array("i", [0] * world)
