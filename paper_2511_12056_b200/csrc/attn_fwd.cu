@@ -5,8 +5,10 @@
 // which is Alg. 1 line 3 `attention(Q[:,j],K[:,j],V[:,j])` for a
 // group of heads; the scale 1/sqrt(D) is the north star's (R1).
 //
-// Design, one CTA = one 128-row query tile of one (b, head); clusters of two CTAs
-// (adjacent query tiles of the same head) share every K/V tile through TMA multicast.
+// Design, one CTA = one 128-row query tile of one (b, head); the two CTAs of a cluster
+// (adjacent query tiles of the same head) form a CTA PAIR that runs every MMA as one tcgen05 cta_group::2
+// instruction (M = 256): each CTA holds its own Q tile and only HALF of every K tile (64 keys) and V tile
+// (D/2 columns), so each SM takes in half of the K/V stream; only the leader CTA issues MMAs.
 //   * TMEM: three S buffers (fp32, 128 columns each) at [0,128), [128,256), [256,384) and ONE O
 //     accumulator at [384, 384+D).  KV tile j goes to S buffer j%3 and is handled by softmax group j%3
 //     (groups = warps 4g..4g+3, one warp per TMEM lane quarter = SM sub-partition).  Three S buffers make
@@ -21,11 +23,13 @@
 //     O in TMEM before releasing P(j).  Each group keeps its own partial row sum l_g relative to the last
 //     max it saw; the epilogue merges them.
 //   warp 12 TMA producer (warps 13, 14 idle): Q once, then K/V tiles through an NS-slot smem ring in consumption order
-//           (K0, K1, K2, V0, K3, V1, K4, ...); each CTA of the cluster (CL CTAs) fetches 128/CL of the rows of
-//           every tile and multicasts them to all of them.
-//   warp 15 TMEM allocator + tcgen05.mma issuer (one elected lane; highest warp id = scheduler priority):
-//           S(j) = Q K_j^T (SS, M=N=128) into S buffer j%3; O += P(j) V_j (TS: P from TMEM, V MN-major,
-//           N = D in one instruction), released in two key halves; S(j+3) is issued right after PV(j).
+//           (K0, K1, K2, V0, K3, V1, K4, ...); each CTA of the pair loads only its half of every tile (64 keys
+//           of K, D/2 columns of V), counted on the leader's full barrier.
+//   warp 15 TMEM allocator (cta_group::2, both CTAs) + tcgen05.mma issuer (leader CTA, one elected lane; highest
+//           warp id = scheduler priority): S(j) = Q K_j^T (SS, M=256, N=128) into S buffer j%3 of both CTAs;
+//           O += P(j) V_j (TS: P from each CTA's TMEM, V MN-major, N = D in one instruction), released in two
+//           key halves once the softmax warps of BOTH CTAs arrived (8 arrivals on the leader's barrier);
+//           S(j+3) is issued right after PV(j).  Commits are multicast to both CTAs' barriers.
 //   * softmax (one thread per row, 128 keys): two-pass over TMEM (row max, then exp2 in two 64-key halves,
 //     each released to the MMA issuer as soon as its bf16 P is in TMEM, written over scores already read);
 //     fp32, base 2 with log2(e)/sqrt(D) folded into one FFMA2; a quarter of the exponentials run as a
@@ -60,16 +64,11 @@ constexpr int MMA_WARP = NUM_SOFTMAX_WARPS + 3;
 constexpr int NUM_WARPS = NUM_SOFTMAX_WARPS + 4;
 constexpr int NUM_THREADS = NUM_WARPS * 32;
 constexpr int SOFTMAX_REGS = 152, AUX_REGS = 56;
-constexpr float RESCALE_TAU = 8.0f;
-// CTAs per cluster: adjacent query tiles of one head; each CTA fetches 1/CL of the rows of every K/V tile and
-// multicasts them to the whole cluster (L2->SMEM traffic per query row / CL).
-#ifdef SPA_CLUSTER
-constexpr int CL = SPA_CLUSTER;
-#else
-constexpr int CL = 2;
-#endif
-static_assert(CL == 1 || CL == 2 || CL == 4, "cluster size");
-constexpr uint16_t CL_MASK = (uint16_t)((1u << CL) - 1);  // log2 domain: raise the running max only if it grows by > 2^8
+constexpr float RESCALE_TAU = 8.0f;   // log2 domain: raise the running max only if it grows by > 2^8
+// CTA pair: clusters of 2 adjacent query tiles of one head run every MMA as ONE cta_group::2 instruction
+// (M = 256); each CTA holds only half of every K tile (64 keys) and half of every V tile (D/2 columns), so
+// each SM takes in half of the K/V stream (the L2->SMEM feed was the first limiter of the M = 128 design).
+constexpr uint16_t PAIR_MASK = 0x3;
 // named barriers: 0 = __syncthreads; 1 + 3*wq + g = "running max of the previous tile is in xm[] for the
 // warp of group g on lane quarter wq"; 1 + 3*4 = all softmax warps (epilogue merge).
 constexpr uint32_t BAR_EPI = 1 + 3 * 4;
@@ -94,23 +93,22 @@ struct Cfg {
     static constexpr int N128 = D / 64;                  // 1, 1, 2
     static constexpr int N64 = (D % 64) ? 1 : 0;         // 0, 1, 0
     static constexpr int NCHUNK = N128 + N64;
-    // V tiles (MN-major B operand of PV, N = D in ONE instruction): D=64/128 -> 64-column SW128 atoms,
-    // D=96 -> three 32-column SW64 atoms; LBO = distance between atoms along N.
-    static constexpr bool V_SW64 = (D == 96);
-    static constexpr int V_ATOM_COLS = V_SW64 ? 32 : 64;
-    static constexpr int V_ATOMS = D / V_ATOM_COLS;
+    // This CTA's half of a V tile (MN-major B operand of PV; the pair's N = D is split D/2 per CTA), as
+    // [128 keys][D/2] in swizzle atoms along N: D=128 -> one 64-column SW128 atom, D=64 -> one 32-column SW64
+    // atom, D=96 -> three 16-column SW32 atoms; LBO = distance between atoms along N.
+    static constexpr int VH = D / 2;
+    static constexpr int V_ATOM_COLS = (D == 128) ? 64 : (D == 64 ? 32 : 16);
+    static constexpr uint32_t V_LAYOUT = (D == 128) ? 2u : (D == 64 ? 4u : 6u);   // SW128 / SW64 / SW32
+    static constexpr int V_ATOMS = VH / V_ATOM_COLS;
     static constexpr int V_ATOM_BYTES = BM * V_ATOM_COLS * 2;
-    static constexpr int TILE_BYTES = BM * D * 2;
+    static constexpr int TILE_BYTES = BM * D * 2;        // Q tile; a whole K or V tile of the pair
+    static constexpr int HALF_BYTES = TILE_BYTES / 2;    // one ring slot: this CTA's half of a K or V tile
+    static constexpr int KCHUNK = (BN / 2) * 128;        // K half: 64 keys; 64-column SW128 chunk c at c*KCHUNK
     // K/V ring slots (as many as fit: the ring depth is the TMA lookahead that hides L2 latency)
-#if defined(SPA_NS128) && defined(SPA_NS96)
-    static constexpr int NS = (D == 128) ? SPA_NS128 : (D == 96 ? SPA_NS96 : 8);
-#else
-    static constexpr int NS = (D == 128) ? 6 : 8;
-#endif
-    static constexpr int SMEM_TILES = 1 + NS;
+    static constexpr int NS = (D == 128) ? 12 : 16;
     static constexpr int BAR_BYTES = 512;
     static constexpr int XCH_BYTES = BM * 4;   // static smem: running max (the epilogue's (m, l) reuse ring slot 0)
-    static constexpr int SMEM_BYTES = 1024 /*align slack*/ + SMEM_TILES * TILE_BYTES + BAR_BYTES;
+    static constexpr int SMEM_BYTES = 1024 /*align slack*/ + TILE_BYTES + NS * HALF_BYTES + BAR_BYTES;
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr uint32_t O_COL = 128 * NG;          // O accumulator columns [O_COL, O_COL + D)
     static_assert(O_COL + D <= TMEM_COLS, "TMEM budget");
@@ -123,18 +121,18 @@ struct Cfg {
     static constexpr int POLY_FROM = 12;
 #endif
     static_assert(SMEM_BYTES + XCH_BYTES <= 227 * 1024, "shared memory");
-    static_assert(NS <= 8, "barrier block");
-    static_assert(2 * NG * BM * 4 <= TILE_BYTES, "epilogue exchange fits in a ring slot");
+    static_assert(NS <= 16, "barrier block");
+    static_assert(2 * NG * BM * 4 <= HALF_BYTES, "epilogue exchange fits in a ring slot");
 };
 
 __device__ __forceinline__ int chunk_off(int c) { return c * (BM * 128); }  // Q/K chunk c byte offset in a tile
 
 struct SmemBars {
     uint64_t q_full;
-    uint64_t kv_full[8];
-    uint64_t kv_empty[8];
+    uint64_t kv_full[16];      // leader's count the data of both CTAs' halves (follower's unused)
+    uint64_t kv_empty[16];
     uint64_t s_full[NG];       // [buffer]: S(j) complete
-    uint64_t p_full[NG][2];    // [buffer][key half]: P(j) half written by the 4 warps of that group
+    uint64_t p_full[NG][2];    // [buffer][key half]: P(j) half written (leader's: 4 warps of the group in each CTA)
     uint64_t pv_done[NG];      // [buffer]: PV(j) complete (O may be rescaled)
     uint64_t o_final;          // all PVs completed (epilogue)
     uint32_t tmem_base;
@@ -171,9 +169,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     using C = Cfg<D>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t *sQ = smem;                                        // 1 tile
-    uint8_t *sKV = smem + C::TILE_BYTES;                       // NS tiles
-    SmemBars *bars = reinterpret_cast<SmemBars *>(smem + C::SMEM_TILES * C::TILE_BYTES);
+    uint8_t *sQ = smem;                                        // this CTA's Q tile
+    uint8_t *sKV = smem + C::TILE_BYTES;                       // NS half tiles
+    SmemBars *bars = reinterpret_cast<SmemBars *>(smem + C::TILE_BYTES + C::NS * C::HALF_BYTES);
     __shared__ float xm[BM];            // running max handed from the group of tile j-1 to the group of tile j
     // epilogue: xml[g] = last max seen by group g, xml[NG + g] = its partial sum; in ring slot 0, which is idle once
     // every MMA of this CTA completed (o_final): all loads into this CTA's ring were consumed by then.
@@ -197,12 +195,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mbar_init(&bars->q_full, 1);
         for (int i = 0; i < C::NS; ++i) {
             ptx::mbar_init(&bars->kv_full[i], 1);
-            ptx::mbar_init(&bars->kv_empty[i], CL);   // released by the MMA issuers of every CTA of the cluster
+            ptx::mbar_init(&bars->kv_empty[i], 1);   // the leader's commit, multicast to both CTAs
         }
         for (int t = 0; t < NG; ++t) {
             ptx::mbar_init(&bars->s_full[t], 1);
-            ptx::mbar_init(&bars->p_full[t][0], 4);   // one arrival per softmax warp of that group
-            ptx::mbar_init(&bars->p_full[t][1], 4);
+            ptx::mbar_init(&bars->p_full[t][0], 8);   // one arrival per softmax warp of that group, both CTAs
+            ptx::mbar_init(&bars->p_full[t][1], 8);
             ptx::mbar_init(&bars->pv_done[t], 1);
         }
         ptx::mbar_init(&bars->o_final, 1);
@@ -212,54 +210,53 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::prefetch_tmap(&tmQa); ptx::prefetch_tmap(&tmKa); ptx::prefetch_tmap(&tmVa);
         if (C::N64) { ptx::prefetch_tmap(&tmQb); ptx::prefetch_tmap(&tmKb); }
     }
-    if (warp == MMA_WARP) {
-        ptx::tmem_alloc(&bars->tmem_base, C::TMEM_COLS);
-        ptx::tmem_relinquish();
+    if (warp == MMA_WARP) {   // same warp id in both CTAs (cta_group::2 allocation)
+        ptx::tmem_alloc2(&bars->tmem_base, C::TMEM_COLS);
+        ptx::tmem_relinquish2();
     }
     ptx::tc_fence_before();
     __syncthreads();
-    ptx::cluster_sync();   // the partner's barriers exist before any multicast lands in its shared memory
+    ptx::cluster_sync();   // the peer's barriers exist before any TMA / commit / arrive targets them
     ptx::tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
-    const uint32_t crank = CL > 1 ? ptx::cluster_ctarank() : 0;   // which 128/CL rows of each K/V tile it fetches
+    const uint32_t crank = ptx::cluster_ctarank();   // 0 = leader (issues the pair's MMAs)
 
     if (warp == PRODUCER_WARP) {
         // ------------------------------------------------------------ TMA producer
         ptx::setmaxnreg_dec<AUX_REGS>();
         const uint64_t pol_q = ptx::policy_evict_first();
         const uint64_t pol_kv = ptx::policy_evict_last();
+        // Every load of either CTA is counted on the LEADER's barrier, which expects the pair's bytes.
         if (lane == 0 && n_kv > 0) {
-            ptx::mbar_arrive_expect_tx(&bars->q_full, C::TILE_BYTES);
-            ptx::tma_load_4d(&tmQa, &bars->q_full, sQ, 0, head, qtile * BM, b, pol_q);
-            if (C::N128 == 2) ptx::tma_load_4d(&tmQa, &bars->q_full, sQ + chunk_off(1), 64, head, qtile * BM, b, pol_q);
-            if (C::N64) ptx::tma_load_4d(&tmQb, &bars->q_full, sQ + chunk_off(1), 64, head, qtile * BM, b, pol_q);
+            const uint32_t qbar = ptx::mapa(&bars->q_full, 0);
+            if (crank == 0) ptx::mbar_arrive_expect_tx(&bars->q_full, 2 * C::TILE_BYTES);
+            ptx::tma_load_4d_2sm(&tmQa, qbar, sQ, 0, head, qtile * BM, b, pol_q);
+            if (C::N128 == 2) ptx::tma_load_4d_2sm(&tmQa, qbar, sQ + chunk_off(1), 64, head, qtile * BM, b, pol_q);
+            if (C::N64) ptx::tma_load_4d_2sm(&tmQb, qbar, sQ + chunk_off(1), 64, head, qtile * BM, b, pol_q);
         }
         int cnt = 0;
-        // Each CTA of the cluster fetches rows [crank*RB, crank*RB + RB) of every K/V tile and multicasts them to
-        // all CTAs (same smem offset); each CTA's kv_full expects the whole tile.
-        constexpr int RB = BN / CL;
-        auto tload = [&](const CUtensorMap *m, uint64_t *bar, uint8_t *dst, int c0, int row) {
-            if (CL == 1) ptx::tma_load_4d(m, bar, dst, c0, head, row, b, pol_kv);
-            else ptx::tma_load_4d_mc(m, bar, dst, c0, head, row, b, CL_MASK, pol_kv);
-        };
+        // K half: keys [j*128 + 64*crank, +64) of tile j, all D columns; V half: all 128 keys, columns
+        // [crank*D/2, +D/2).  A slot is refilled once the pair's MMA that read it completed (kv_empty).
         auto load = [&](bool isV, int j) {
             const int slot = cnt % C::NS;
             ptx::mbar_wait(&bars->kv_empty[slot], ((cnt / C::NS) & 1) ^ 1);
             if (lane == 0) {
-                uint8_t *dst = sKV + slot * C::TILE_BYTES;
-                uint64_t *bar = &bars->kv_full[slot];
-                ptx::mbar_arrive_expect_tx(bar, C::TILE_BYTES);
+                uint8_t *dst = sKV + slot * C::HALF_BYTES;
+                const uint32_t bar = ptx::mapa(&bars->kv_full[slot], 0);
+                if (crank == 0) ptx::mbar_arrive_expect_tx(&bars->kv_full[slot], C::TILE_BYTES);
+                auto tl = [&](const CUtensorMap *m, uint8_t *d, int c0, int row) {
+                    ptx::tma_load_4d_2sm(m, bar, d, c0, head, row, b, pol_kv);
+                };
                 TRACE(j, isV ? 12 : 11);
-                const int row = j * BN + (int)crank * RB;
                 if (isV) {
 #pragma unroll
                     for (int a = 0; a < C::V_ATOMS; ++a)
-                        tload(&tmVa, bar, dst + a * C::V_ATOM_BYTES + crank * (C::V_ATOM_BYTES / CL), a * C::V_ATOM_COLS,
-                              row);
+                        tl(&tmVa, dst + a * C::V_ATOM_BYTES, (int)crank * C::VH + a * C::V_ATOM_COLS, j * BN);
                 } else {
-                    tload(&tmKa, bar, dst + crank * RB * 128, 0, row);
-                    if (C::N128 == 2) tload(&tmKa, bar, dst + chunk_off(1) + crank * RB * 128, 64, row);
-                    if (C::N64) tload(&tmKb, bar, dst + chunk_off(1) + crank * RB * 64, 64, row);
+                    const int row = j * BN + (int)crank * (BN / 2);
+                    tl(&tmKa, dst, 0, row);
+                    if (C::N128 == 2) tl(&tmKa, dst + C::KCHUNK, 64, row);
+                    if (C::N64) tl(&tmKb, dst + C::KCHUNK, 64, row);
                 }
             }
             __syncwarp();
@@ -274,8 +271,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     } else if (warp == MMA_WARP) {
         // ------------------------------------------------------------ MMA issuer
         ptx::setmaxnreg_dec<AUX_REGS>();
-        constexpr uint32_t IDESC_QK = ptx::idesc_bf16(BM, BN, 0, 0);
-        constexpr uint32_t IDESC_PV = ptx::idesc_bf16(BM, D, 0, 1);
+        constexpr uint32_t IDESC_QK = ptx::idesc_bf16(2 * BM, BN, 0, 0);   // the pair: M = 256
+        constexpr uint32_t IDESC_PV = ptx::idesc_bf16(2 * BM, D, 0, 1);
         const uint32_t qa = ptx::smem_u32(sQ);
         const uint32_t sKV_addr = ptx::smem_u32(sKV);
 
@@ -290,17 +287,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // Descriptors are built once; per MMA only the 14-bit start-address field moves (+byte offset >> 4).
         const uint64_t dQ128 = ptx::smem_desc(qa, 16, 1024, 2), dQ64 = ptx::smem_desc(qa + chunk_off(1), 16, 512, 4);
         const uint64_t dK128 = ptx::smem_desc(sKV_addr, 16, 1024, 2);
-        const uint64_t dK64 = ptx::smem_desc(sKV_addr + chunk_off(1), 16, 512, 4);
+        const uint64_t dK64 = ptx::smem_desc(sKV_addr + C::KCHUNK, 16, 512, 4);
         constexpr uint32_t rowb = C::V_ATOM_COLS * 2;
-        const uint64_t dV = ptx::smem_desc(sKV_addr, C::V_ATOM_BYTES, 8 * rowb, C::V_SW64 ? 4u : 2u);
-        const bool leader = ptx::elect_one();
+        const uint64_t dV = ptx::smem_desc(sKV_addr, C::V_ATOM_BYTES, 8 * rowb, C::V_LAYOUT);
+        // only the leader CTA issues (one elected lane); the follower's MMA warp just owns its TMEM allocation
+        const bool leader = (crank == 0) && ptx::elect_one();
         const uint32_t tO = tmem + C::O_COL;
         // S(j) = Q K_j^T into S buffer j%NG: K-major A (Q) and B (K), 16-element k-steps per swizzle chunk.
         auto issue_qk = [&](int j) {
             const int slot = acquire();
             if (leader) {
                 TRACE(j, 2);
-                const uint64_t so = (uint64_t)(slot * C::TILE_BYTES) >> 4;
+                const uint64_t so = (uint64_t)(slot * C::HALF_BYTES) >> 4;
                 const uint32_t d = tmem + (j % NG) * 128;
 #pragma unroll
                 for (int c = 0; c < C::NCHUNK; ++c) {
@@ -308,49 +306,50 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const int ksteps = sw64 ? 2 : 4;
 #pragma unroll
                     for (int kk = 0; kk < ksteps; ++kk) {
-                        const uint64_t off = (uint64_t)((sw64 ? 0 : c * (BM * 128)) + kk * 32) >> 4;
-                        ptx::mma_ss(d, (sw64 ? dQ64 : dQ128) + off, (sw64 ? dK64 : dK128) + so + off, IDESC_QK,
-                                    (c | kk) ? 1u : 0u);
+                        const uint64_t qoff = (uint64_t)((sw64 ? 0 : c * (BM * 128)) + kk * 32) >> 4;
+                        const uint64_t koff = (uint64_t)((sw64 ? 0 : c * C::KCHUNK) + kk * 32) >> 4;
+                        ptx::mma_ss2(d, (sw64 ? dQ64 : dQ128) + qoff, (sw64 ? dK64 : dK128) + so + koff, IDESC_QK,
+                                     (c | kk) ? 1u : 0u);
                     }
                 }
-                ptx::mma_commit(&bars->s_full[j % NG]);
-                if (CL == 1) ptx::mma_commit(&bars->kv_empty[slot]);
-                else ptx::mma_commit_mc(&bars->kv_empty[slot], CL_MASK);
+                ptx::mma_commit2_mc(&bars->s_full[j % NG], PAIR_MASK);
+                ptx::mma_commit2_mc(&bars->kv_empty[slot], PAIR_MASK);
             }
             __syncwarp();
         };
 
-        if (n_kv > 0) ptx::mbar_wait(&bars->q_full, 0);
-        for (int j = 0; j < NG && j < n_kv; ++j) issue_qk(j);
-        for (int j = 0; j < n_kv; ++j) {
-            const int t = j % NG;
-            const uint32_t tS = tmem + t * 128;
-            const int slotV = acquire();
-            if (leader) TRACE(j, 10);
-            const uint64_t dVs = dV + ((uint64_t)(slotV * C::TILE_BYTES) >> 4);
+        if (crank == 0) {
+            if (n_kv > 0) ptx::mbar_wait(&bars->q_full, 0);
+            for (int j = 0; j < NG && j < n_kv; ++j) issue_qk(j);
+            for (int j = 0; j < n_kv; ++j) {
+                const int t = j % NG;
+                const uint32_t tS = tmem + t * 128;
+                const int slotV = acquire();
+                if (leader) TRACE(j, 10);
+                const uint64_t dVs = dV + ((uint64_t)(slotV * C::HALF_BYTES) >> 4);
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                ptx::mbar_wait(&bars->p_full[t][hf], (j / NG) & 1);
-                ptx::tc_fence_after();
-                if (leader) {
-                    TRACE(j, hf);
-                    // O (+)= P(j)[keys 64hf..64hf+63] V_j[those keys]; that P half sits in columns 64hf..64hf+31
+                for (int hf = 0; hf < 2; ++hf) {
+                    ptx::mbar_wait(&bars->p_full[t][hf], (j / NG) & 1);   // both CTAs' softmax warps
+                    ptx::tc_fence_after();
+                    if (leader) {
+                        TRACE(j, hf);
+                        // O (+)= P(j)[keys 64hf..64hf+63] V_j[those keys]; that P half sits in columns 64hf..64hf+31
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const int key16 = hf * 4 + kk;
-                        ptx::mma_ts(tO, tS + hf * 64 + kk * 8, dVs + ((uint64_t)(key16 * 16 * rowb) >> 4), IDESC_PV,
-                                    (j > 0 || key16 > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const int key16 = hf * 4 + kk;
+                            ptx::mma_ts2(tO, tS + hf * 64 + kk * 8, dVs + ((uint64_t)(key16 * 16 * rowb) >> 4),
+                                         IDESC_PV, (j > 0 || key16 > 0) ? 1u : 0u);
+                        }
+                        if (hf == 1) {
+                            ptx::mma_commit2_mc(&bars->kv_empty[slotV], PAIR_MASK);
+                            ptx::mma_commit2_mc(&bars->pv_done[t], PAIR_MASK);
+                            if (j == n_kv - 1) ptx::mma_commit2_mc(&bars->o_final, PAIR_MASK);
+                        }
                     }
-                    if (hf == 1) {
-                        if (CL == 1) ptx::mma_commit(&bars->kv_empty[slotV]);
-                        else ptx::mma_commit_mc(&bars->kv_empty[slotV], CL_MASK);
-                        ptx::mma_commit(&bars->pv_done[t]);
-                        if (j == n_kv - 1) ptx::mma_commit(&bars->o_final);
-                    }
+                    __syncwarp();
                 }
-                __syncwarp();
+                if (j + NG < n_kv) issue_qk(j + NG);
             }
-            if (j + NG < n_kv) issue_qk(j + NG);
         }
     } else if (warp < NUM_SOFTMAX_WARPS) {
         // ------------------------------------------------------------ softmax / correction / epilogue
@@ -481,7 +480,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ptx::tmem_wait_st();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&bars->p_full[g][h]);
+                if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(&bars->p_full[g][h], 0));   // the leader's
                 if (tr && h == 0) TRACE(j, 8);
             }
             {
@@ -541,10 +540,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     ptx::tc_fence_before();
     __syncthreads();
-    ptx::cluster_sync();   // no CTA leaves while its partner may still multicast into it / arrive on its barriers
+    ptx::cluster_sync();   // no CTA leaves while its peer may still signal its barriers or read its smem / TMEM
     if (warp == MMA_WARP) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+        ptx::tmem_dealloc2(tmem, C::TMEM_COLS);
     }
 }
 
@@ -566,8 +565,9 @@ EncodeTiledFn get_encode_fn() {
 }
 
 // 4-D map over a [B][S][heads][D] bf16 view: dims (D, heads, S, B), box (box_d, 1, box_rows, 1).
+// swz = swizzle width in bytes (32, 64 or 128) = the UMMA layout the box lands in.
 bool make_map(CUtensorMap *m, const void *base, int D, int heads, int S, int B, long long tok_stride,
-              long long batch_stride, int box_d, bool sw64, int box_rows = BM) {
+              long long batch_stride, int box_d, int swz, int box_rows = BM) {
     EncodeTiledFn enc = get_encode_fn();
     if (!enc) return false;
     cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)heads, (cuuint64_t)S, (cuuint64_t)B};
@@ -576,7 +576,8 @@ bool make_map(CUtensorMap *m, const void *base, int D, int heads, int S, int B, 
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     sw64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     swz == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : (swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -585,17 +586,17 @@ template <int D>
 cudaError_t launch_d(const AttnProblem &p, cudaStream_t st) {
     using C = Cfg<D>;
     // m[0]/m[1]: Q 64-col SW128 / 32-col SW64 boxes of 128 rows; m[2]/m[3]: the same for K with 64-row boxes
-    // (each CTA of a cluster fetches 128/CL rows of a tile); m[4]: V 64-col SW128 (D=64/128) or 32-col SW64 (D=96) boxes
-    // of 64 rows; m[5] unused.
+    // (a CTA's half of a K tile); m[4]: V boxes of one swizzle atom (64 / 32 / 16 columns for D = 128 / 64 / 96)
+    // by 128 rows (a CTA's half of a V tile is D/2 columns); m[5] unused.
     CUtensorMap m[6];
-    const int vcols = C::V_SW64 ? 32 : 64;
-    bool ok = make_map(&m[0], p.q, D, p.n_heads, p.Sq, p.B, p.q_tok_stride, p.q_batch_stride, 64, false) &&
-              make_map(&m[2], p.k, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, 64, false, BN / CL) &&
-              make_map(&m[4], p.v, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, vcols, C::V_SW64,
-                       BN / CL);
+    const int vswz = C::V_ATOM_COLS * 2;
+    bool ok = make_map(&m[0], p.q, D, p.n_heads, p.Sq, p.B, p.q_tok_stride, p.q_batch_stride, 64, 128) &&
+              make_map(&m[2], p.k, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, 64, 128, BN / 2) &&
+              make_map(&m[4], p.v, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, C::V_ATOM_COLS, vswz,
+                       BN);
     if (ok && C::N64)
-        ok = make_map(&m[1], p.q, D, p.n_heads, p.Sq, p.B, p.q_tok_stride, p.q_batch_stride, 32, true) &&
-             make_map(&m[3], p.k, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, 32, true, BN / CL);
+        ok = make_map(&m[1], p.q, D, p.n_heads, p.Sq, p.B, p.q_tok_stride, p.q_batch_stride, 32, 64) &&
+             make_map(&m[3], p.k, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, 32, 64, BN / 2);
     else {
         m[1] = m[0];
         m[3] = m[2];
@@ -617,17 +618,17 @@ cudaError_t launch_d(const AttnProblem &p, cudaStream_t st) {
     a.Skv = p.Skv;
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
     a.kv_len = p.kv_len;
-    // clusters of 2 CTAs (adjacent query tiles of one head) share every K/V tile via TMA multicast;
-    // an odd tile count gets one extra all-out-of-range tile that only helps its partner load.
+    // CTA pairs (adjacent query tiles of one head) run each MMA as one cta_group::2 instruction; an odd tile
+    // count gets one extra all-out-of-range tile (zero-filled Q, rows never stored) to complete the last pair.
     const int qtiles = (p.Sq + BM - 1) / BM;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((qtiles + CL - 1) / CL * CL, p.n_heads, p.B);
+    cfg.gridDim = dim3((qtiles + 1) / 2 * 2, p.n_heads, p.B);
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = C::SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
