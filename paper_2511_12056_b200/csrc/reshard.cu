@@ -9,6 +9,9 @@
 // A job enumerates runs with a 4-level index (i3,i2,i1,i0) and byte strides; each thread moves
 // one 64-byte quad (4 x 16-B vector loads, then 4 x 16-B stores), so reads and writes are
 // coalesced 16-B accesses within runs.  Grid = multiple of the 148 SMs, grid-stride loop.
+// The quad -> (run, i0..i3) decomposition uses 32-bit multiply-high division by host-precomputed
+// magic numbers (64-bit integer division would make the copy ALU-bound: ~26 % ALU, 34 % of HBM
+// peak in profiles/r01_v4/ncu_full_copy_runs.json).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -20,9 +23,24 @@ namespace spa {
 
 namespace {
 
+// n / d for any 32-bit n as (umulhi(n, m) + n) >> l, with l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1
+struct FastDiv {
+    uint32_t d, m, l;
+};
+FastDiv make_fastdiv(uint32_t d) {
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    const uint64_t m = ((1ull << 32) * ((1ull << l) - d)) / d + 1;
+    return FastDiv{d, (uint32_t)m, l};
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
+    return (uint32_t)(((uint64_t)__umulhi(n, f.m) + n) >> f.l);
+}
+
 struct JobPack {
     CopyJob job[kMaxCopyJobs];
     long long quad_end[kMaxCopyJobs];  // exclusive prefix sums of quads per job
+    FastDiv qpr[kMaxCopyJobs], c3[kMaxCopyJobs], c2[kMaxCopyJobs], c1[kMaxCopyJobs];
     int n;
 };
 
@@ -47,16 +65,17 @@ __global__ void __launch_bounds__(256) copy_runs_kernel(const __grid_constant__ 
         while (q >= jp.quad_end[job]) ++job;
         while (job > 0 && q < jp.quad_end[job - 1]) --job;
         const CopyJob &J = jp.job[job];
-        const long long local = q - (job ? jp.quad_end[job - 1] : 0);
-        const long long qpr = J.run_bytes >> 6;
-        long long run = local / qpr;
-        const long long qq = local - run * qpr;
-        const long long i0 = run % J.count[3];
-        run /= J.count[3];
-        const long long i1 = run % J.count[2];
-        run /= J.count[2];
-        const long long i2 = run % J.count[1];
-        const long long i3 = run / J.count[1];
+        const uint32_t local = (uint32_t)(q - (job ? jp.quad_end[job - 1] : 0));   // < 2^32 (host-checked)
+        uint32_t run = fdiv(local, jp.qpr[job]);
+        const uint32_t qq = local - run * jp.qpr[job].d;
+        uint32_t nx = fdiv(run, jp.c3[job]);
+        const uint32_t i0 = run - nx * jp.c3[job].d;
+        run = nx;
+        nx = fdiv(run, jp.c2[job]);
+        const uint32_t i1 = run - nx * jp.c2[job].d;
+        run = nx;
+        const uint32_t i3 = fdiv(run, jp.c1[job]);
+        const uint32_t i2 = run - i3 * jp.c1[job].d;
         const uint8_t *s = J.src + i3 * J.src_stride[0] + i2 * J.src_stride[1] + i1 * J.src_stride[2] +
                            i0 * J.src_stride[3] + qq * 64;
         uint8_t *d = J.dst + i3 * J.dst_stride[0] + i2 * J.dst_stride[1] + i1 * J.dst_stride[2] +
@@ -84,8 +103,14 @@ cudaError_t launch_copy_jobs(const CopyJob *jobs, int n, cudaStream_t st, int *l
             const CopyJob &J = jobs[i];
             long long runs = J.count[0] * J.count[1] * J.count[2] * J.count[3];
             if (runs <= 0 || J.run_bytes <= 0) continue;
+            const long long quads = runs * (J.run_bytes >> 6);
+            if (quads >= (1ll << 32)) return cudaErrorInvalidValue;   // 32-bit quad index per job (256 GB)
             jp.job[m] = J;
-            acc += runs * (J.run_bytes >> 6);
+            jp.qpr[m] = make_fastdiv((uint32_t)(J.run_bytes >> 6));
+            jp.c3[m] = make_fastdiv((uint32_t)J.count[3]);
+            jp.c2[m] = make_fastdiv((uint32_t)J.count[2]);
+            jp.c1[m] = make_fastdiv((uint32_t)J.count[1]);
+            acc += quads;
             jp.quad_end[m] = acc;
             ++m;
         }
