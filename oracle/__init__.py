@@ -21,5 +21,5 @@ brute force, library routines); see DESIGN.md §Oracle pins.  No function is
 """
 from . import attention, sp  # noqa: F401
 from .attention import (attention_rows, softmax_weights, mha_unsharded, build_library,  # noqa: F401
-                        key_valid_from_lengths,
+                        key_valid_from_lengths, attention_rows_lse,
                         library_path)

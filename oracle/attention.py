@@ -51,6 +51,9 @@ def _load():
         lib.oracle_attention_rows_masked.argtypes = [dp, ctypes.c_long, ctypes.c_long, dp, dp, ctypes.c_long,
                                                      ctypes.c_long, u8p, dp, ctypes.c_long, ctypes.c_int]
         lib.oracle_attention_rows_masked.restype = ctypes.c_int
+        lib.oracle_attention_rows_lse.argtypes = [dp, ctypes.c_long, ctypes.c_long, dp, dp, ctypes.c_long,
+                                                  ctypes.c_long, u8p, dp, ctypes.c_long, dp, ctypes.c_int]
+        lib.oracle_attention_rows_lse.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -95,6 +98,26 @@ def attention_rows(q: np.ndarray, K: np.ndarray, V: np.ndarray, nthreads: Option
     if rc != 0:
         raise RuntimeError(f"oracle_attention_rows failed ({rc})")
     return out
+
+
+def attention_rows_lse(q: np.ndarray, K: np.ndarray, V: np.ndarray, nthreads: Optional[int] = None,
+                       key_valid: Optional[np.ndarray] = None):
+    """(O [R,D], lse [R]): attention_rows and lse[r] = ln sum_t exp(q_r . k_t / sqrt(D)) over the valid keys
+    (-inf when none) -- what partial softmaxes over disjoint key blocks combine with (R21)."""
+    q, K, V = _f64c(q), _f64c(K), _f64c(V)
+    R, D = q.shape
+    S = K.shape[0]
+    out = np.empty((R, D), dtype=np.float64)
+    lse = np.empty(R, dtype=np.float64)
+    kvp = None
+    if key_valid is not None:
+        kv = np.ascontiguousarray(np.asarray(key_valid, dtype=bool).astype(np.uint8))
+        kvp = kv.ctypes.data_as(ctypes.POINTER(ctypes.c_ubyte))
+    rc = _load().oracle_attention_rows_lse(_dptr(q), R, D, _dptr(K), _dptr(V), S, D, kvp, _dptr(out), D, _dptr(lse),
+                                           int(nthreads or default_threads()))
+    if rc != 0:
+        raise RuntimeError("oracle_attention_rows_lse failed")
+    return out, lse
 
 
 def softmax_weights(q: np.ndarray, K: np.ndarray) -> np.ndarray:

@@ -38,8 +38,19 @@
  * paper never defines it -- DESIGN.md reading R2/R20): a masked key takes no part in the softmax,
  * i.e. z[t] = -inf, e[t] = 0.  A row with no valid key gets w = 0 everywhere (its output is 0).
  */
+static int softmax_weights_lse(const double *q, const double *K, long S, long D, const unsigned char *key_valid,
+                               double *w, double *lse_out);
+
 int oracle_softmax_weights_masked(const double *q, const double *K, long S, long D, const unsigned char *key_valid,
                                   double *w)
+{
+    return softmax_weights_lse(q, K, S, D, key_valid, w, NULL);
+}
+
+/* ... and lse = ln sum_t exp(z[t]) = m + ln l over the valid keys (-inf if none): the quantity two partial
+ * softmaxes over disjoint key blocks are combined with (ring attention, R21). */
+static int softmax_weights_lse(const double *q, const double *K, long S, long D, const unsigned char *key_valid,
+                               double *w, double *lse_out)
 {
     if (!q || !K || !w || S <= 0 || D <= 0) return 1;
     double sqrt_d = sqrt((double)D);
@@ -53,6 +64,7 @@ int oracle_softmax_weights_masked(const double *q, const double *K, long S, long
     }
     if (m == -INFINITY) {           /* no valid key */
         for (long t = 0; t < S; ++t) w[t] = 0.0;
+        if (lse_out) *lse_out = -INFINITY;
         return 0;
     }
     double l = 0.0;
@@ -61,6 +73,7 @@ int oracle_softmax_weights_masked(const double *q, const double *K, long S, long
         l += w[t];
     }
     for (long t = 0; t < S; ++t) w[t] = w[t] / l;
+    if (lse_out) *lse_out = m + log(l);
     return 0;
 }
 
@@ -71,9 +84,9 @@ int oracle_softmax_weights(const double *q, const double *K, long S, long D, dou
 
 /* One output row: out[D] = sum_t w[t] V[t,:] (t ascending). scratch has S doubles. */
 static void attention_one_row(const double *q, const double *K, const double *V, long S, long D,
-                              const unsigned char *key_valid, double *out, double *scratch)
+                              const unsigned char *key_valid, double *out, double *lse, double *scratch)
 {
-    oracle_softmax_weights_masked(q, K, S, D, key_valid, scratch);
+    softmax_weights_lse(q, K, S, D, key_valid, scratch, lse);
     for (long d = 0; d < D; ++d) out[d] = 0.0;
     for (long t = 0; t < S; ++t) {
         double wt = scratch[t];
@@ -86,6 +99,7 @@ typedef struct {
     const double *Q, *K, *V;
     const unsigned char *key_valid;
     double *O;
+    double *lse;     /* optional [nq] */
     long nq, S, D;
     long q_stride, o_stride; /* elements between consecutive query / output rows */
     int tid, nthreads;
@@ -99,7 +113,7 @@ static void *rows_worker(void *arg)
     if (!scratch) { j->err = 2; return NULL; }
     for (long r = j->tid; r < j->nq; r += j->nthreads)
         attention_one_row(j->Q + r * j->q_stride, j->K, j->V, j->S, j->D, j->key_valid, j->O + r * j->o_stride,
-                          scratch);
+                          j->lse ? j->lse + r : NULL, scratch);
     free(scratch);
     return NULL;
 }
@@ -109,9 +123,21 @@ static void *rows_worker(void *arg)
  * (key_valid NULL = all keys).  Q rows at stride q_stride, out rows at o_stride; K, V dense [S][D].
  * nthreads <= 0 -> 1.  Returns 0 on success.
  */
+int oracle_attention_rows_lse(const double *Q, long nq, long q_stride, const double *K, const double *V,
+                              long S, long D, const unsigned char *key_valid, double *out, long o_stride,
+                              double *lse, int nthreads);
+
 int oracle_attention_rows_masked(const double *Q, long nq, long q_stride, const double *K, const double *V,
                                  long S, long D, const unsigned char *key_valid, double *out, long o_stride,
                                  int nthreads)
+{
+    return oracle_attention_rows_lse(Q, nq, q_stride, K, V, S, D, key_valid, out, o_stride, NULL, nthreads);
+}
+
+/* As above, and lse[r] = ln sum_t exp(z[r][t]) over the valid keys (lse may be NULL). */
+int oracle_attention_rows_lse(const double *Q, long nq, long q_stride, const double *K, const double *V,
+                              long S, long D, const unsigned char *key_valid, double *out, long o_stride,
+                              double *lse, int nthreads)
 {
     if (!Q || !K || !V || !out || S <= 0 || D <= 0 || nq < 0) return 1;
     if (nthreads <= 0) nthreads = 1;
@@ -120,7 +146,7 @@ int oracle_attention_rows_masked(const double *Q, long nq, long q_stride, const 
     pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
     if (!jobs || !th) { free(jobs); free(th); return 2; }
     for (int i = 0; i < nthreads; ++i) {
-        jobs[i] = (rows_job){Q, K, V, key_valid, out, nq, S, D, q_stride, o_stride, i, nthreads, 0};
+        jobs[i] = (rows_job){Q, K, V, key_valid, out, lse, nq, S, D, q_stride, o_stride, i, nthreads, 0};
         if (nthreads == 1) rows_worker(&jobs[i]);
         else pthread_create(&th[i], NULL, rows_worker, &jobs[i]);
     }

@@ -142,6 +142,49 @@ def padded_forward(Qs, Ks, Vs, n_owners: int, forward) -> List[np.ndarray]:
     return [np.ascontiguousarray(o[:, :, :H]) for o in outs]
 
 
+# ---------------------------------------------------------------- Ring attention (USP fallback)
+def lse_merge(parts, lses):
+    """Combine softmax-normalised partial results over disjoint key blocks (R21):
+    O = sum_i exp(lse_i - M) O_i / sum_i exp(lse_i - M), M = max_i lse_i; lse = M + ln sum_i exp(lse_i - M).
+    parts[i]: [..., D], lses[i]: [...] (float64).  Rows with every lse = -inf give 0 and lse -inf."""
+    L = np.stack(lses)                      # [n, ...]
+    M = L.max(axis=0)
+    finite = np.isfinite(M)
+    Ms = np.where(finite, M, 0.0)
+    W = np.where(np.isfinite(L), np.exp(L - Ms), 0.0)
+    den = W.sum(axis=0)
+    num = sum(W[i][..., None] * parts[i] for i in range(len(parts)))
+    out = np.where(finite[..., None], num / np.where(finite, den, 1.0)[..., None], 0.0)
+    lse = np.where(finite, Ms + np.log(np.where(finite, den, 1.0)), -np.inf)
+    return out, lse
+
+
+def ring_forward(Qs, Ks, Vs, attn_lse) -> List[np.ndarray]:
+    """Ring attention over P ranks (the paper's Ring-Attention fallback when H is not divisible, PAPER.md:171;
+    it gives no procedure -- DESIGN.md R21): rank r keeps its query shard and all heads; at step t it attends
+    to the K/V shard of rank (r - t) mod P (the shards travel around the ring r -> r+1), giving a partial
+    result and its lse per row; the P partials are combined with lse_merge.  attn_lse(q [R,D], K, V) ->
+    (O [R,D], lse [R]).  No head divisibility is needed."""
+    P = len(Qs)
+    B, S_l, H, D = Qs[0].shape
+    outs = []
+    for r in range(P):
+        parts, lses = [], []
+        for t in range(P):
+            src = (r - t) % P
+            O = np.empty((B, S_l, H, D))
+            L = np.empty((B, S_l, H))
+            for b in range(B):
+                for k in range(H):
+                    O[b, :, k], L[b, :, k] = attn_lse(np.ascontiguousarray(Qs[r][b, :, k]),
+                                                      np.ascontiguousarray(Ks[src][b, :, k]),
+                                                      np.ascontiguousarray(Vs[src][b, :, k]))
+            parts.append(O)
+            lses.append(L)
+        outs.append(lse_merge(parts, lses)[0])
+    return outs
+
+
 # ---------------------------------------------------------------- attention per rank
 def _attn_heads(Rq: np.ndarray, Rk: np.ndarray, Rv: np.ndarray, rows: np.ndarray, heads: Sequence[int],
                 attn: Attn) -> np.ndarray:
