@@ -95,6 +95,10 @@ typedef struct {
                        Hp = spa_pad_heads(H, nranks); rank r owns padded heads [r*Hp/nranks, (r+1)*Hp/nranks);
                        pad heads are never read from q/k/v, never computed and never written to out
                        (user buffers keep H heads).  DESIGN.md R10. */
+    int ring;       /* 0: Ulysses / PipeSP / Aco plan.  1: Ring-Attention plan ("switch ... from
+                       Ulysses to Ring-Attention ... avoiding the overhead of padding"; R21): every
+                       rank keeps all H heads of its sequence shard, only S % nranks == 0 is required (any H);
+                       use spa_ring_attention*.  stages, n_src and pad_heads must be 0 / 1 / 0. */
 } spa_shape;
 
 /* Validates everything synchronously.  Requirements: D in {64,96,128}; S % n_src == 0;
@@ -159,6 +163,17 @@ spa_status spa_pipesp_attention_local(spa_plan *plan, const void *const q[], con
                                       const void *const v[], void *const out[], void *ws, void *stream);
 spa_status spa_aco_attention_local(spa_plan *plan, const void *const q[], const void *const k[],
                                    const void *const v[], void *const out[], void *ws, void *stream);
+
+/* Ring attention (shape.ring = 1; R21): q, k, v, out as above ([B, S/P, H, D], any H).  Rank r
+ * attends to the K/V shard of rank (r - t) mod P at step t; the shards travel the ring r-1 -> r -> r+1 on
+ * the comm stream (double-buffered, NCCL send/recv) while the previous block is computed; each step writes
+ * an fp32 partial result and its per-row log-sum-exp into ws, and a merge kernel combines the P partials
+ * (softmax over the union of the blocks).  Not bit-identical to the Ulysses path (a different summation
+ * order), within the same tolerance of the fp64 definition.  Key-padding masks: SPA_ERR_UNSUPPORTED. */
+spa_status spa_ring_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out, void *ws,
+                              void *stream);
+spa_status spa_ring_attention_local(spa_plan *plan, const void *const q[], const void *const k[],
+                                    const void *const v[], void *const out[], void *ws, void *stream);
 
 /* ------------------------------------------------------------------ building blocks (bit-exact tests)
  * seq->head reshard ("all_to_all"): x [B,S/P,H,D] ->

@@ -511,8 +511,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const float inv = n_kv > 0 ? 1.f / lsum : 0.f;   // no valid key: the row is 0 (R20)
         const long long srow = (long long)qtile * BM + row;
         const bool valid = srow < args.Sq;      // tcgen05.ld is warp-collective: every lane loads, valid lanes store
-        uint4 *dst = reinterpret_cast<uint4 *>(args.O + (long long)b * args.o_batch_stride + srow * args.o_tok_stride +
-                                               (long long)head * D);
+        const long long oidx = (long long)b * args.o_batch_stride + srow * args.o_tok_stride + (long long)head * D;
+        uint4 *dst = reinterpret_cast<uint4 *>(args.O + oidx);
+        // ring / merge support: the row's log-sum-exp of the scaled scores, ln sum_t exp(q.k_t / sqrt(D)) =
+        // (running max + log2 l) * ln 2 in the kernel's base-2 domain; -inf for a row without valid keys
+        if (args.lse && valid && g == 0)
+            args.lse[((long long)b * args.Sq + srow) * args.lse_heads + head] =
+                n_kv > 0 ? (mm + __log2f(lsum)) * 0.69314718055994531f : -INFINITY;
         // this warp normalises and stores the 16-column chunks c with c % NG == g
 #pragma unroll
         for (int c = 0; c < C::OCHUNKS; ++c) {
@@ -525,6 +530,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             } else {
 #pragma unroll
                 for (int u = 0; u < 16; ++u) r[u] = 0u;
+            }
+            if (args.O32) {   // fp32 output (partial results of ring attention, merged by spa_lse_merge)
+                if (valid) {
+                    float4 *d4 = reinterpret_cast<float4 *>(args.O32 + oidx + col);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        d4[u] = make_float4(__uint_as_float(r[4 * u]) * inv, __uint_as_float(r[4 * u + 1]) * inv,
+                                            __uint_as_float(r[4 * u + 2]) * inv, __uint_as_float(r[4 * u + 3]) * inv);
+                }
+                continue;
             }
             uint32_t w[8];
 #pragma unroll
@@ -618,6 +633,9 @@ cudaError_t launch_d(const AttnProblem &p, cudaStream_t st) {
     a.Skv = p.Skv;
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
     a.kv_len = p.kv_len;
+    a.O32 = reinterpret_cast<float *>(p.o32);
+    a.lse = p.lse;
+    a.lse_heads = p.n_heads;
     // CTA pairs (adjacent query tiles of one head) run each MMA as one cta_group::2 instruction; an odd tile
     // count gets one extra all-out-of-range tile (zero-filled Q, rows never stored) to complete the last pair.
     const int qtiles = (p.Sq + BM - 1) / BM;

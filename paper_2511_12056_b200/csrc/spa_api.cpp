@@ -91,6 +91,10 @@ struct spa_plan {
     int h = 1, S_l = 1;
     int Hp = 1;     // heads after padding to a multiple of P (== sh.H unless shape.pad_heads)
     const int32_t *kv_len = nullptr;   // key-padding lengths, device int32 [B] (spa_plan_set_kv_len) or NULL
+    // ring plans (shape.ring = 1; R21): per-rank workspace = 2 K/V receive slots + P fp32 partials + lse
+    bool ring = false;
+    long long E_loc = 0;                         // B * S_l * H * D
+    long long off_kvbuf = 0, off_parts = 0, off_lse = 0;
     Split split;
     // per-rank workspace layout (bytes)
     long long E_src = 0, E_own = 0;  // elements of one send-side / owner-side tensor
@@ -568,6 +572,7 @@ spa_status prepare(spa_plan *p, Exec &x, void *ws, void *stream, bool local) {
 
 spa_status attention_call(spa_plan *p, int nsrc_ptrs, const void *const q[], const void *const k[],
                           const void *const v[], void *const out[], void *ws, void *stream, bool local, bool ulysses) {
+    if (p && p->ring) return fail(SPA_ERR_INVALID, "ring plan: use spa_ring_attention");
     Exec x{};
     SPA_TRY(prepare(p, x, ws, stream, local));
     Split one = make_split(p->h, p->S_l, 1);
@@ -714,6 +719,27 @@ spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *sha
     if (Psrc < 1 || Psrc > P) return fail(SPA_ERR_SHAPE, "n_src must be in [0, nranks]");
     if (s.S % Psrc) return fail(SPA_ERR_SHAPE, "S must be divisible by the number of source ranks");
     if (s.pad_heads != 0 && s.pad_heads != 1) return fail(SPA_ERR_INVALID, "pad_heads must be 0 or 1");
+    if (s.ring != 0 && s.ring != 1) return fail(SPA_ERR_INVALID, "ring must be 0 or 1");
+    if (s.ring) {
+        // Ring attention: every rank keeps all heads; only S % P matters.
+        if (s.n_src != 0 && s.n_src != P) return fail(SPA_ERR_SHAPE, "ring plans have no co-processor ranks");
+        if (s.S % P) return fail(SPA_ERR_SHAPE, "S must be divisible by nranks");
+        spa_plan *p = new spa_plan;
+        p->comm = comm; p->sh = s; p->P = P; p->Psrc = P; p->ring = true;
+        p->Hp = s.H; p->h = s.H; p->S_l = s.S / P;
+        p->split = make_split(1, p->S_l, 1);
+        p->E_loc = (long long)s.B * p->S_l * s.H * s.D;
+        long long off = 0;
+        auto take = [&](long long bytes) { long long o = off; off = align_up(off + bytes, 256); return o; };
+        if (P > 1) {
+            p->off_kvbuf = take(4 * p->E_loc * 2);                        // [slot 0/1][K/V] bf16
+            p->off_parts = take((long long)P * p->E_loc * 4);             // [P] fp32 partial O
+            p->off_lse = take((long long)P * (p->E_loc / s.D) * 4);       // [P] fp32 lse
+        }
+        p->ws_rank_bytes = off;
+        *plan = p;
+        return SPA_OK;
+    }
     if (s.H % P && !s.pad_heads)
         return fail(SPA_ERR_SHAPE, "H must be divisible by nranks (or set shape.pad_heads = 1)");
     spa_plan *p = new spa_plan;
@@ -824,6 +850,7 @@ spa_status spa_aco_attention(spa_plan *plan, const void *q, const void *k, const
     if (!plan) return fail(SPA_ERR_INVALID, "plan is NULL");
     if (plan->Psrc == plan->P) return fail(SPA_ERR_INVALID, "not an Aco plan (n_src must be < nranks)");
     if (plan->coproc_busy) return fail(SPA_ERR_BUSY, "co-processor group busy");
+    if (plan->ring) return fail(SPA_ERR_INVALID, "ring plan: use spa_ring_attention");
     const bool src = plan->comm->kind == KIND_NCCL && is_source(plan, plan->comm->rank);
     if (!src) {
         if (q || k || v || out) return fail(SPA_ERR_INVALID, "co-processor ranks pass NULL q/k/v/out");
@@ -853,8 +880,110 @@ spa_status spa_aco_attention_local(spa_plan *plan, const void *const q[], const 
     return attention_call(plan, n_local_srcs(plan), q, k, v, out, ws, stream, true, false);
 }
 
+// ------------------------------------------------------------------ ring attention (R21)
+// Rank r keeps its query shard and all heads; at step t it attends to the K/V shard of rank (r - t) mod P, which
+// travels the ring r-1 -> r -> r+1 on the comm stream while the previous block is being computed (double-buffered
+// receive slots); every step writes an fp32 partial O and its per-row lse, and lse_merge combines the P partials.
+static AttnProblem ring_problem(const spa_plan *p, const void *q, const void *k, const void *v, float *o32,
+                                float *lse) {
+    AttnProblem a{};
+    const long long tok = (long long)p->sh.H * p->sh.D;
+    a.q = q; a.k = k; a.v = v; a.o = nullptr; a.o32 = o32; a.lse = lse;
+    a.B = p->sh.B; a.Sq = a.Skv = p->S_l; a.n_heads = p->sh.H; a.D = p->sh.D;
+    a.q_tok_stride = a.kv_tok_stride = a.o_tok_stride = tok;
+    a.q_batch_stride = a.kv_batch_stride = a.o_batch_stride = (long long)p->S_l * tok;
+    a.kv_len = nullptr;   // a key-padding mask is global-position based: not supported on ring plans
+    return a;
+}
+
+static spa_status ring_call(spa_plan *p, int n, const void *const q[], const void *const k[], const void *const v[],
+                            void *const out[], void *ws, void *stream, bool local) {
+    if (!p) return fail(SPA_ERR_INVALID, "plan is NULL");
+    if (!p->ring) return fail(SPA_ERR_INVALID, "not a ring plan (shape.ring = 1)");
+    if (p->kv_len) return fail(SPA_ERR_UNSUPPORTED, "key-padding masks are not supported on ring plans");
+    Exec x{};
+    SPA_TRY(prepare(p, x, ws, stream, local));
+    for (int i = 0; i < n; ++i) {
+        SPA_TRY(check_ptr(q[i], "q")); SPA_TRY(check_ptr(k[i], "k"));
+        SPA_TRY(check_ptr(v[i], "v")); SPA_TRY(check_ptr(out[i], "out"));
+    }
+    p->attn_launches = 0;
+    p->copy_launches = 0;
+    const int P = p->P;
+    const long long tok = (long long)p->sh.H * p->sh.D;
+    cudaStream_t sc = x.sc;
+    if (P == 1) {   // one block: the plain kernel
+        AttnProblem a = ring_problem(p, q[0], k[0], v[0], nullptr, nullptr);
+        a.o = out[0]; a.o32 = nullptr;
+        SPA_CHECK_CUDA(launch_attention(a, sc));
+        ++p->attn_launches;
+        return SPA_OK;
+    }
+    const long long rows = p->E_loc / p->sh.D;
+    auto parts = [&](int r) { return reinterpret_cast<float *>(resolve(x, r, BUF_WS, p->off_parts)); };
+    auto lses = [&](int r) { return reinterpret_cast<float *>(resolve(x, r, BUF_WS, p->off_lse)); };
+    auto merge = [&](int r, void *o) -> spa_status {
+        SPA_CHECK_CUDA(launch_lse_merge(parts(r), p->E_loc, lses(r), rows, P, p->sh.B, p->S_l, p->sh.H, p->sh.D, o,
+                                        tok, (long long)p->S_l * tok, sc));
+        ++p->copy_launches;
+        return SPA_OK;
+    };
+    if (p->comm->kind == KIND_LOOPBACK) {
+        // virtual ranks on one GPU: step t of rank r reads rank (r - t) mod P's shard in place (the ring's data
+        // movement is the identity here; the arithmetic and the merge are the multi-GPU ones)
+        for (int r = 0; r < P; ++r) {
+            for (int t = 0; t < P; ++t) {
+                const int src = ((r - t) % P + P) % P;
+                AttnProblem a = ring_problem(p, q[r], k[src], v[src], parts(r) + t * p->E_loc, lses(r) + t * rows);
+                SPA_CHECK_CUDA(launch_attention(a, sc));
+                ++p->attn_launches;
+            }
+            SPA_TRY(merge(r, out[r]));
+        }
+        return SPA_OK;
+    }
+    // NCCL: compute on the caller's stream, K/V blocks around the ring on the comm stream
+    SPA_TRY(ensure_stream(p->comm));
+    cudaStream_t sm = p->comm->stream;
+    SPA_TRY(ensure_events(p, 4 + 2 * (size_t)P, 0));
+    cudaEvent_t *ev = p->sync_ev.data();
+    cudaEvent_t ev_entry = ev[0], ev_done = ev[1];
+    cudaEvent_t *comp = ev + 4, *comm = ev + 4 + P;
+    const int r = p->comm->rank, next = (r + 1) % P, prev = (r + P - 1) % P;
+    const size_t blk = (size_t)p->E_loc * 2;
+    uint8_t *kvbuf = resolve(x, r, BUF_WS, p->off_kvbuf);
+    auto slotK = [&](int s) { return kvbuf + (size_t)(2 * s) * blk; };
+    auto slotV = [&](int s) { return kvbuf + (size_t)(2 * s + 1) * blk; };
+    SPA_CHECK_CUDA(cudaEventRecord(ev_entry, sc));
+    SPA_CHECK_CUDA(cudaStreamWaitEvent(sm, ev_entry, 0));
+    for (int t = 0; t < P; ++t) {
+        const void *ck = t == 0 ? k[0] : slotK((t - 1) & 1);
+        const void *cv = t == 0 ? v[0] : slotV((t - 1) & 1);
+        if (t + 1 < P) {   // comm step t: pass the current block on, receive the next one
+            if (t >= 1) SPA_CHECK_CUDA(cudaStreamWaitEvent(sm, comp[t - 1], 0));   // slot t%2 was read at step t-1
+            SPA_CHECK_NCCL(ncclGroupStart());
+            SPA_CHECK_NCCL(ncclSend(ck, blk, ncclUint8, next, p->comm->nccl, sm));
+            SPA_CHECK_NCCL(ncclSend(cv, blk, ncclUint8, next, p->comm->nccl, sm));
+            SPA_CHECK_NCCL(ncclRecv(slotK(t & 1), blk, ncclUint8, prev, p->comm->nccl, sm));
+            SPA_CHECK_NCCL(ncclRecv(slotV(t & 1), blk, ncclUint8, prev, p->comm->nccl, sm));
+            SPA_CHECK_NCCL(ncclGroupEnd());
+            SPA_CHECK_CUDA(cudaEventRecord(comm[t], sm));
+        }
+        if (t >= 1) SPA_CHECK_CUDA(cudaStreamWaitEvent(sc, comm[t - 1], 0));
+        AttnProblem a = ring_problem(p, q[0], ck, cv, parts(r) + t * p->E_loc, lses(r) + t * rows);
+        SPA_CHECK_CUDA(launch_attention(a, sc));
+        ++p->attn_launches;
+        SPA_CHECK_CUDA(cudaEventRecord(comp[t], sc));
+    }
+    SPA_TRY(merge(r, out[0]));
+    SPA_CHECK_CUDA(cudaEventRecord(ev_done, sm));
+    SPA_CHECK_CUDA(cudaStreamWaitEvent(sc, ev_done, 0));
+    return SPA_OK;
+}
+
 static spa_status reshard_call(spa_plan *plan, int n, const void *const x[], void *const xh[], void *ws, void *stream,
                                bool local, bool to_head) {
+    if (plan && plan->ring) return fail(SPA_ERR_INVALID, "ring plan: no reshard");
     Exec e{};
     SPA_TRY(prepare(plan, e, ws, stream, local));
     if (plan->Psrc != plan->P) return fail(SPA_ERR_INVALID, "reshard needs n_src == nranks");
@@ -878,6 +1007,16 @@ static spa_status reshard_call(spa_plan *plan, int n, const void *const x[], voi
         e.o_send_buf = BUF_XHEAD;
     }
     return execute(e);
+}
+
+spa_status spa_ring_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out, void *ws,
+                              void *stream) {
+    return ring_call(plan, 1, &q, &k, &v, &out, ws, stream, false);
+}
+spa_status spa_ring_attention_local(spa_plan *plan, const void *const q[], const void *const k[],
+                                    const void *const v[], void *const out[], void *ws, void *stream) {
+    if (!plan || !q || !k || !v || !out) return fail(SPA_ERR_INVALID, "NULL argument");
+    return ring_call(plan, plan->P, q, k, v, out, ws, stream, true);
 }
 
 spa_status spa_reshard_seq_to_head(spa_plan *plan, const void *x, void *x_head, void *ws, void *stream) {
@@ -933,6 +1072,7 @@ spa_status spa_attention_fwd(const void *q, const void *k, const void *v, void *
 // ------------------------------------------------------------------ describe (host only)
 spa_status spa_plan_describe_pack(const spa_plan *plan, int rank, spa_copy_desc *out, int max, int *n) {
     if (!plan || !n) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (plan->ring) return fail(SPA_ERR_INVALID, "ring plan: nothing to describe");
     *n = 0;
     if (plan->P == 1 || !is_source(plan, rank)) return SPA_OK;
     const long long offs[3] = {plan->off_sendQ, plan->off_sendK, plan->off_sendV};
@@ -951,6 +1091,7 @@ spa_status spa_plan_describe_pack(const spa_plan *plan, int rank, spa_copy_desc 
 
 spa_status spa_plan_describe_unpack(const spa_plan *plan, int rank, spa_copy_desc *out, int max, int *n) {
     if (!plan || !n) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (plan->ring) return fail(SPA_ERR_INVALID, "ring plan: nothing to describe");
     *n = 0;
     if (plan->P == 1 || !is_source(plan, rank)) return SPA_OK;
     std::vector<CopyJob> jobs;
@@ -966,6 +1107,7 @@ spa_status spa_plan_describe_unpack(const spa_plan *plan, int rank, spa_copy_des
 spa_status spa_plan_describe_messages(const spa_plan *plan, int stage, int dir, int rank, spa_msg *out, int max,
                                       int *n) {
     if (!plan || !n) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (plan->ring) return fail(SPA_ERR_INVALID, "ring plan: nothing to describe");
     if (stage < 0 || stage >= plan->split.n() || rank < 0 || rank >= plan->P)
         return fail(SPA_ERR_INVALID, "bad stage/rank");
     std::vector<Msg> m;
@@ -981,6 +1123,7 @@ spa_status spa_plan_describe_messages(const spa_plan *plan, int stage, int dir, 
 
 spa_status spa_plan_describe_attention(const spa_plan *p, int stage, int rank, spa_attn_desc *out) {
     if (!p || !out) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (p->ring) return fail(SPA_ERR_INVALID, "ring plan: nothing to describe");
     if (stage < 0 || stage >= p->split.n() || rank < 0 || rank >= p->P) return fail(SPA_ERR_INVALID, "bad stage/rank");
     const Split &s = p->split;
     const int kh = stage / s.C, c = stage % s.C;

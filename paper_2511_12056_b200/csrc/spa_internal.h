@@ -17,6 +17,8 @@ struct AttnProblem {
     long long kv_tok_stride, kv_batch_stride;
     long long o_tok_stride, o_batch_stride;
     const int32_t *kv_len = nullptr;   // key padding: device int32 [B], keys t >= kv_len[b] masked (NULL: none)
+    void *o32 = nullptr;               // non-NULL: fp32 output instead of o (same element strides)
+    float *lse = nullptr;              // non-NULL: per-row log-sum-exp, [B][Sq][n_heads] contiguous
 };
 
 // Kernel-side arguments (tensor maps travel separately as __grid_constant__ parameters).
@@ -26,7 +28,17 @@ struct AttnArgs {
     int Sq, Skv;
     float scale_log2;
     const int32_t *kv_len;   // NULL or device [B]
+    float *O32;              // NULL or fp32 output
+    float *lse;              // NULL or [B][Sq][lse_heads]
+    int lse_heads;
 };
+
+// out[b, s, j, :] = sum_i w_i O_i[b, s, j, :] / sum_i w_i, w_i = exp(lse_i - max_i lse_i), over n partial results
+// O_i (fp32, [B][Sq][n_heads][D] contiguous, at parts + i*part_stride elements) with lse_i ([B][Sq][n_heads] at
+// lses + i*lse_stride); out bf16 with token / batch strides (elements).  Rows whose every lse is -inf are 0.
+cudaError_t launch_lse_merge(const float *parts, long long part_stride, const float *lses, long long lse_stride,
+                             int n, int B, int Sq, int n_heads, int D, void *out, long long o_tok_stride,
+                             long long o_batch_stride, cudaStream_t st);
 
 cudaError_t launch_attention(const AttnProblem &p, cudaStream_t st);
 

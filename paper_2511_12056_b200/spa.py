@@ -17,6 +17,7 @@ __all__ = [
     "SpaError", "load", "header_functions", "get_unique_id", "Comm", "Plan", "Shape", "Profile",
     "spa_attention_fwd", "spa_attention_fwd_masked", "spa_pipesp_attention", "spa_ulysses_attention", "spa_aco_attention",
     "spa_pipesp_attention_local", "spa_ulysses_attention_local", "spa_aco_attention_local",
+    "spa_ring_attention", "spa_ring_attention_local",
     "spa_reshard_seq_to_head", "spa_reshard_head_to_seq", "spa_reshard_seq_to_head_local",
     "spa_reshard_head_to_seq_local", "spa_pad_heads", "attention", "BUF_Q", "BUF_K", "BUF_V", "BUF_OUT",
     "BUF_WS", "SPA_OPT_PROFILE", "SPA_OPT_SKIP_COMM", "SPA_OPT_COPROC_BUSY",
@@ -35,7 +36,8 @@ class SpaError(RuntimeError):
 
 class Shape(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int), ("S", ctypes.c_int), ("H", ctypes.c_int), ("D", ctypes.c_int),
-                ("stages", ctypes.c_int), ("n_src", ctypes.c_int), ("pad_heads", ctypes.c_int)]
+                ("stages", ctypes.c_int), ("n_src", ctypes.c_int), ("pad_heads", ctypes.c_int),
+                ("ring", ctypes.c_int)]
 
 
 class Profile(ctypes.Structure):
@@ -109,6 +111,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "spa_ulysses_attention_local": ([_P, _PP, _PP, _PP, _PP, _P, _P], i),
         "spa_pipesp_attention_local": ([_P, _PP, _PP, _PP, _PP, _P, _P], i),
         "spa_aco_attention_local": ([_P, _PP, _PP, _PP, _PP, _P, _P], i),
+        "spa_ring_attention": ([_P, _P, _P, _P, _P, _P, _P], i),
+        "spa_ring_attention_local": ([_P, _PP, _PP, _PP, _PP, _P, _P], i),
         "spa_reshard_seq_to_head": ([_P, _P, _P, _P, _P], i),
         "spa_reshard_head_to_seq": ([_P, _P, _P, _P, _P], i),
         "spa_reshard_seq_to_head_local": ([_P, _PP, _PP, _P, _P], i),
@@ -224,9 +228,9 @@ class Comm:
 
 class Plan:
     def __init__(self, comm: Comm, B: int, S: int, H: int, D: int, stages: int = 1, n_src: int = 0,
-                 pad_heads: bool = False):
+                 pad_heads: bool = False, ring: bool = False):
         self.comm = comm
-        self.shape = Shape(B, S, H, D, stages, n_src, int(bool(pad_heads)))
+        self.shape = Shape(B, S, H, D, stages, n_src, int(bool(pad_heads)), int(bool(ring)))
         h = ctypes.c_void_p()
         _check(load().spa_plan_create(ctypes.byref(h), comm.h, ctypes.byref(self.shape)), "spa_plan_create")
         self.h = h
@@ -360,6 +364,16 @@ def spa_pipesp_attention_local(plan: Plan, qs, ks, vs, outs, ws, stream=None):
 def spa_aco_attention_local(plan: Plan, qs, ks, vs, outs, ws, stream=None):
     _check(load().spa_aco_attention_local(plan.h, _arr(qs), _arr(ks), _arr(vs), _arr(outs), _ptr(ws),
                                           _stream(stream)), "spa_aco_attention_local")
+
+
+def spa_ring_attention(plan: Plan, q, k, v, out, ws, stream=None):
+    _check(load().spa_ring_attention(plan.h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(ws), _stream(stream)),
+           "spa_ring_attention")
+
+
+def spa_ring_attention_local(plan: Plan, qs, ks, vs, outs, ws, stream=None):
+    _check(load().spa_ring_attention_local(plan.h, _arr(qs), _arr(ks), _arr(vs), _arr(outs), _ptr(ws),
+                                           _stream(stream)), "spa_ring_attention_local")
 
 
 def spa_reshard_seq_to_head(plan: Plan, x, x_head, ws, stream=None):

@@ -75,6 +75,23 @@ def test_host_path_padded_heads(P, H, S, B, stages):
             assert plans[r].describe_attention(k, r).n_heads == max(0, min(g, H - (r * h + kh * g)))
 
 
+def test_ring_plan_validation_and_workspace():
+    """Ring plans (R21): any H, S % P == 0; workspace = 2 K/V slots + P fp32 partials + lse."""
+    P, B, S, H, D = 4, 2, 4 * 96, 5, 96
+    p = spa.Plan(spa.Comm.host(P, 1), B, S, H, D, ring=True)
+    E = B * (S // P) * H * D
+    assert p.workspace_bytes >= 4 * E * 2 + P * E * 4 + P * (E // D) * 4
+    with pytest.raises(spa.SpaError) as e:
+        spa.Plan(spa.Comm.host(P, 0), B, S + 1, H, D, ring=True)
+    assert e.value.status == 2
+    with pytest.raises(spa.SpaError) as e:   # Ulysses / PipeSP calls refuse a ring plan before anything else
+        spa.spa_pipesp_attention(p, 16, 16, 16, 16, 16, stream=0)
+    assert e.value.status == 1
+    with pytest.raises(spa.SpaError):
+        p.describe_messages(0, 0, 1)
+    assert spa.Plan(spa.Comm.host(1, 0), B, S, H, D, ring=True).workspace_bytes == 0
+
+
 def test_host_comm_cannot_execute():
     comm = spa.Comm.host(2, 1)
     plan = spa.Plan(comm, 1, 256, 4, 64, stages=2)
