@@ -164,6 +164,15 @@ spa_status spa_pipesp_attention_local(spa_plan *plan, const void *const q[], con
 spa_status spa_aco_attention_local(spa_plan *plan, const void *const q[], const void *const k[],
                                    const void *const v[], void *const out[], void *ws, void *stream);
 
+/* Single-GPU attention from and to HOST memory (pinned for overlap; 1-rank loopback plan): q, k, v, o are host
+ * [B, S, H, D] bf16; ws = device workspace of spa_plan_host_workspace_bytes() (device copies of Q, K, V, O).
+ * The plan's `stages` sets the head-group count G_h = gcd(stages, H): the H2D copy of group i+1's columns
+ * and the D2H copy of group i-1's output overlap group i's attention (two extra streams; the output is in
+ * `o` when `stream` reaches the end of the call).  Same result bits as spa_attention_fwd on those heads. */
+spa_status spa_plan_host_workspace_bytes(const spa_plan *plan, size_t *bytes);
+spa_status spa_attention_host(spa_plan *plan, const void *q, const void *k, const void *v, void *o, void *ws,
+                              void *stream);
+
 /* Ring attention (shape.ring = 1; R21): q, k, v, out as above ([B, S/P, H, D], any H).  Rank r
  * attends to the K/V shard of rank (r - t) mod P at step t; the shards travel the ring r-1 -> r -> r+1 on
  * the comm stream (double-buffered, NCCL send/recv) while the previous block is computed; each step writes

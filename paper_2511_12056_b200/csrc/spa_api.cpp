@@ -1009,6 +1009,72 @@ static spa_status reshard_call(spa_plan *plan, int n, const void *const x[], voi
     return execute(e);
 }
 
+// ------------------------------------------------------------------ single GPU from / to host memory
+// Head group i (g heads, G_h = gcd(stages, H) groups): H2D of its Q/K/V columns (2-D strided copies) on one
+// stream, its attention on the caller's stream, D2H of its O columns on a third: group i's attention overlaps
+// group i+1's H2D and group i-1's D2H (the copy engines run both directions at once).
+spa_status spa_plan_host_workspace_bytes(const spa_plan *plan, size_t *bytes) {
+    if (!plan || !bytes) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (plan->P != 1 || plan->ring) return fail(SPA_ERR_INVALID, "host-buffer calls need a 1-rank, non-ring plan");
+    *bytes = (size_t)4 * plan->sh.B * plan->sh.S * plan->sh.H * plan->sh.D * 2;
+    return SPA_OK;
+}
+
+spa_status spa_attention_host(spa_plan *p, const void *q, const void *k, const void *v, void *o, void *ws,
+                              void *stream) {
+    if (!p || !q || !k || !v || !o || !ws) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (p->P != 1 || p->ring || p->comm->kind != KIND_LOOPBACK)
+        return fail(SPA_ERR_INVALID, "host-buffer calls need a 1-rank loopback plan");
+    SPA_TRY(check_ptr(ws, "ws"));
+    SPA_CHECK_CUDA(cudaSetDevice(p->comm->device));
+    cudaStream_t sc = reinterpret_cast<cudaStream_t>(stream);
+    SPA_TRY(ensure_stream(p->comm));
+    cudaStream_t s_out = p->comm->stream;
+    if (!p->sc_alt) SPA_CHECK_CUDA(cudaStreamCreateWithFlags(&p->sc_alt, cudaStreamNonBlocking));
+    cudaStream_t s_in = p->sc_alt;
+    const int B = p->sh.B, S = p->sh.S, H = p->sh.H, D = p->sh.D;
+    const int G = p->split.G_h, g = H / G;   // head groups (stages = head-group count; query chunks unused)
+    SPA_TRY(ensure_events(p, 4 + 2 * (size_t)G, 0));
+    cudaEvent_t *ev = p->sync_ev.data();
+    cudaEvent_t ev_entry = ev[0], ev_done = ev[1];
+    cudaEvent_t *ev_in = ev + 4, *ev_comp = ev + 4 + G;
+    p->attn_launches = 0;
+    p->copy_launches = 0;
+    const size_t row = (size_t)H * D * 2, grow = (size_t)g * D * 2, rows = (size_t)B * S;
+    const size_t tensor = (size_t)B * S * H * D * 2, group = rows * grow;
+    uint8_t *w = reinterpret_cast<uint8_t *>(ws);
+    uint8_t *dX[4] = {w, w + tensor, w + 2 * tensor, w + 3 * tensor};   // Q, K, V, O: [G][B][S][g][D]
+    const uint8_t *hX[3] = {reinterpret_cast<const uint8_t *>(q), reinterpret_cast<const uint8_t *>(k),
+                            reinterpret_cast<const uint8_t *>(v)};
+    SPA_CHECK_CUDA(cudaEventRecord(ev_entry, sc));
+    SPA_CHECK_CUDA(cudaStreamWaitEvent(s_in, ev_entry, 0));
+    SPA_CHECK_CUDA(cudaStreamWaitEvent(s_out, ev_entry, 0));
+    for (int i = 0; i < G; ++i) {
+        for (int t = 0; t < 3; ++t)
+            SPA_CHECK_CUDA(cudaMemcpy2DAsync(dX[t] + i * group, grow, hX[t] + i * grow, row, grow, rows,
+                                             cudaMemcpyHostToDevice, s_in));
+        SPA_CHECK_CUDA(cudaEventRecord(ev_in[i], s_in));
+    }
+    for (int i = 0; i < G; ++i) {
+        SPA_CHECK_CUDA(cudaStreamWaitEvent(sc, ev_in[i], 0));
+        AttnProblem a{};
+        a.q = dX[0] + i * group; a.k = dX[1] + i * group; a.v = dX[2] + i * group; a.o = dX[3] + i * group;
+        a.B = B; a.Sq = a.Skv = S; a.n_heads = g; a.D = D;
+        a.q_tok_stride = a.kv_tok_stride = a.o_tok_stride = (long long)g * D;
+        a.q_batch_stride = a.kv_batch_stride = a.o_batch_stride = (long long)S * g * D;
+        a.kv_len = p->kv_len;
+        SPA_CHECK_CUDA(launch_attention(a, sc));
+        ++p->attn_launches;
+        SPA_CHECK_CUDA(cudaEventRecord(ev_comp[i], sc));
+        SPA_CHECK_CUDA(cudaStreamWaitEvent(s_out, ev_comp[i], 0));
+        SPA_CHECK_CUDA(cudaMemcpy2DAsync(reinterpret_cast<uint8_t *>(o) + i * grow, row, dX[3] + i * group, grow, grow,
+                                         rows, cudaMemcpyDeviceToHost, s_out));
+    }
+    SPA_CHECK_CUDA(cudaEventRecord(ev_done, s_out));
+    SPA_CHECK_CUDA(cudaStreamWaitEvent(sc, ev_done, 0));
+    return SPA_OK;
+}
+
 spa_status spa_ring_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out, void *ws,
                               void *stream) {
     return ring_call(plan, 1, &q, &k, &v, &out, ws, stream, false);

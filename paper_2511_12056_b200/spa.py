@@ -17,7 +17,7 @@ __all__ = [
     "SpaError", "load", "header_functions", "get_unique_id", "Comm", "Plan", "Shape", "Profile",
     "spa_attention_fwd", "spa_attention_fwd_masked", "spa_pipesp_attention", "spa_ulysses_attention", "spa_aco_attention",
     "spa_pipesp_attention_local", "spa_ulysses_attention_local", "spa_aco_attention_local",
-    "spa_ring_attention", "spa_ring_attention_local",
+    "spa_ring_attention", "spa_ring_attention_local", "spa_attention_host",
     "spa_reshard_seq_to_head", "spa_reshard_head_to_seq", "spa_reshard_seq_to_head_local",
     "spa_reshard_head_to_seq_local", "spa_pad_heads", "attention", "BUF_Q", "BUF_K", "BUF_V", "BUF_OUT",
     "BUF_WS", "SPA_OPT_PROFILE", "SPA_OPT_SKIP_COMM", "SPA_OPT_COPROC_BUSY",
@@ -112,6 +112,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "spa_pipesp_attention_local": ([_P, _PP, _PP, _PP, _PP, _P, _P], i),
         "spa_aco_attention_local": ([_P, _PP, _PP, _PP, _PP, _P, _P], i),
         "spa_ring_attention": ([_P, _P, _P, _P, _P, _P, _P], i),
+        "spa_attention_host": ([_P, _P, _P, _P, _P, _P, _P], i),
+        "spa_plan_host_workspace_bytes": ([_P, ctypes.POINTER(ctypes.c_size_t)], i),
         "spa_ring_attention_local": ([_P, _PP, _PP, _PP, _PP, _P, _P], i),
         "spa_reshard_seq_to_head": ([_P, _P, _P, _P, _P], i),
         "spa_reshard_head_to_seq": ([_P, _P, _P, _P, _P], i),
@@ -263,6 +265,12 @@ class Plan:
         _check(load().spa_plan_last_profile(self.h, ctypes.byref(p)), "spa_plan_last_profile")
         return p
 
+    @property
+    def host_workspace_bytes(self) -> int:
+        n = ctypes.c_size_t()
+        _check(load().spa_plan_host_workspace_bytes(self.h, ctypes.byref(n)), "spa_plan_host_workspace_bytes")
+        return n.value
+
     def workspace(self, device="cuda"):
         import torch
         return torch.empty(max(self.workspace_bytes, 16), dtype=torch.uint8, device=device)
@@ -364,6 +372,12 @@ def spa_pipesp_attention_local(plan: Plan, qs, ks, vs, outs, ws, stream=None):
 def spa_aco_attention_local(plan: Plan, qs, ks, vs, outs, ws, stream=None):
     _check(load().spa_aco_attention_local(plan.h, _arr(qs), _arr(ks), _arr(vs), _arr(outs), _ptr(ws),
                                           _stream(stream)), "spa_aco_attention_local")
+
+
+def spa_attention_host(plan: Plan, q, k, v, o, ws, stream=None):
+    """q, k, v, o: host (pinned) bf16 [B, S, H, D] tensors; ws: device workspace of plan.host_workspace_bytes."""
+    _check(load().spa_attention_host(plan.h, _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(ws), _stream(stream)),
+           "spa_attention_host")
 
 
 def spa_ring_attention(plan: Plan, q, k, v, out, ws, stream=None):

@@ -99,3 +99,18 @@ def test_repeat_determinism_peaky(D, S):
     U.assert_close(first, ref)
     for _ in range(8):
         assert torch.equal(_run(q, k, v).view(torch.int16), first.view(torch.int16))
+
+
+@pytest.mark.parametrize("stages", [1, 3, 4])
+def test_attention_from_host_buffers(stages):
+    """spa_attention_host: pinned host Q/K/V -> host O, pipelined per head group; same bits as the device call."""
+    B, S, H, D = 2, 333, 12, 96
+    q, k, v = U.qkv(B, S, H, D, seed=stages)
+    ref = spa.attention(q, k, v)
+    plan = spa.Plan(spa.Comm.loopback(1), B, S, H, D, stages=stages)
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    ho = torch.full((B, S, H, D), float("nan"), dtype=torch.bfloat16).pin_memory()
+    ws = torch.empty(plan.host_workspace_bytes, dtype=torch.uint8, device="cuda")
+    spa.spa_attention_host(plan, hq, hk, hv, ho, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(ho.view(torch.int16), ref.cpu().view(torch.int16))
