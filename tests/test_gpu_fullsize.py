@@ -110,3 +110,45 @@ def test_fullsize_closed_forms():
     out = spa.attention(q, k, v).double()
     mean = v.double().mean(dim=1, keepdim=True)
     assert (out - mean).abs().max().item() < 1e-3
+
+
+def test_ring_osp_p8_fullsize():
+    """Ring-Attention (R21) at configs[1] size over 8 virtual ranks: sampled rows vs the oracle."""
+    w = synthgen.WORKLOADS["osp480p93f"]
+    q, k, v = _gen(w.B, w.S, w.H, w.D, seed=2)
+    P = 8
+    plan = spa.Plan(spa.Comm.loopback(P), w.B, w.S, w.H, w.D, ring=True)
+    S_l = w.S // P
+    shards = [[x[:, r * S_l:(r + 1) * S_l].contiguous() for r in range(P)] for x in (q, k, v)]
+    outs = [torch.empty_like(t) for t in shards[0]]
+    ws = plan.workspace()
+    spa.spa_ring_attention_local(plan, *shards, outs, ws)
+    torch.cuda.synchronize()
+    del ws
+    out = torch.cat(outs, dim=1)
+    ma, rl = _check_rows(q, k, v, out, _sample(w.S, P, n=32, seed=4), heads=[0, 23])
+    assert ma <= U.MAX_ABS and rl <= U.REL_L2, (ma, rl)
+
+
+def test_key_padding_mask_fullsize():
+    """Key-padding mask (R20) at configs[2] size: kv_len = 70,001 of 76,032 keys, sampled rows vs the oracle on
+    the truncated keys, and the masked PipeSP at P = 4 bit-identical to the masked single-GPU kernel."""
+    w = synthgen.WORKLOADS["hy544p129f"]
+    q, k, v = _gen(w.B, w.S, w.H, w.D, seed=3)
+    L = 70_001
+    kv_len = torch.tensor([L], dtype=torch.int32, device="cuda")
+    single = spa.attention(q, k, v, kv_len=kv_len)
+    torch.cuda.synchronize()
+    ma, rl = _check_rows(q, k[:, :L], v[:, :L], single, _sample(w.S, 4, n=24, seed=5), heads=[7])
+    assert ma <= U.MAX_ABS and rl <= U.REL_L2, (ma, rl)
+    P = 4
+    plan = spa.Plan(spa.Comm.loopback(P), w.B, w.S, w.H, w.D, stages=2)
+    plan.set_kv_len(kv_len)
+    S_l = w.S // P
+    shards = [[x[:, r * S_l:(r + 1) * S_l].contiguous() for r in range(P)] for x in (q, k, v)]
+    outs = [torch.empty_like(t) for t in shards[0]]
+    ws = plan.workspace()
+    spa.spa_pipesp_attention_local(plan, *shards, outs, ws)
+    torch.cuda.synchronize()
+    del ws
+    assert torch.equal(torch.cat(outs, dim=1).view(torch.int16), single.view(torch.int16))

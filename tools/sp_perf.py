@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--stages", default="1,3,24")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--aco", type=int, default=0, help="n_src for an Aco plan (0 = PipeSP)")
+    ap.add_argument("--ring", action="store_true", help="Ring-Attention plan instead of PipeSP")
     args = ap.parse_args()
     w = synthgen.WORKLOADS[args.workload]
     B, S, H, D, P = w.B, w.S, w.H, w.D, args.P
@@ -51,6 +52,22 @@ def main():
     t1 = a.elapsed_time(b) / args.reps
     print(json.dumps({"what": "single kernel, all heads", "ms": t1, "tflops": flops / t1 / 1e9}), flush=True)
     del q_all, k_all, v_all, o_all
+    if args.ring:   # Ring-Attention plan (R21): P x P block attentions + merges, timed as a whole
+        plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, ring=True)
+        ws = plan.workspace()
+        for _ in range(2):
+            spa.spa_ring_attention_local(plan, *shards, outs, ws)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.reps):
+            spa.spa_ring_attention_local(plan, *shards, outs, ws)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / args.reps
+        print(json.dumps({"ring": True, "P": P, "total_ms": ms, "tflops": flops / ms / 1e9}), flush=True)
+        plan.close()
+        return
     for st in [int(x) for x in args.stages.split(",")]:
         plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=st, n_src=args.aco)
         ws = plan.workspace()
