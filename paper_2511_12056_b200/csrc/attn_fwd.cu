@@ -69,6 +69,9 @@ constexpr float RESCALE_TAU = 8.0f;   // log2 domain: raise the running max only
 // (M = 256); each CTA holds only half of every K tile (64 keys) and half of every V tile (D/2 columns), so
 // each SM takes in half of the K/V stream (the L2->SMEM feed was the first limiter of the M = 128 design).
 constexpr uint16_t PAIR_MASK = 0x3;
+// Order in which the softmax releases (and the MMA consumes) the two 64-key halves of P: the upper half first,
+// straight from the registers pass 1 loaded last (one TMEM read of 64 columns per tile saved).
+__device__ constexpr int HALF_ORDER[2] = {1, 0};
 // named barriers: 0 = __syncthreads; 1 + 3*wq + g = "running max of the previous tile is in xm[] for the
 // warp of group g on lane quarter wq"; 1 + 3*4 = all softmax warps (epilogue merge).
 constexpr uint32_t BAR_EPI = 1 + 3 * 4;
@@ -328,19 +331,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (leader) TRACE(j, 10);
                 const uint64_t dVs = dV + ((uint64_t)(slotV * C::HALF_BYTES) >> 4);
 #pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
+                for (int o = 0; o < 2; ++o) {
+                    const int hf = HALF_ORDER[o];   // the key half the softmax releases o-th
                     ptx::mbar_wait(&bars->p_full[t][hf], (j / NG) & 1);   // both CTAs' softmax warps
                     ptx::tc_fence_after();
                     if (leader) {
-                        TRACE(j, hf);
+                        TRACE(j, o);
                         // O (+)= P(j)[keys 64hf..64hf+63] V_j[those keys]; that P half sits in columns 64hf..64hf+31
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             const int key16 = hf * 4 + kk;
                             ptx::mma_ts2(tO, tS + hf * 64 + kk * 8, dVs + ((uint64_t)(key16 * 16 * rowb) >> 4),
-                                         IDESC_PV, (j > 0 || key16 > 0) ? 1u : 0u);
+                                         IDESC_PV, (j > 0 || o > 0 || kk > 0) ? 1u : 0u);
                         }
-                        if (hf == 1) {
+                        if (o == 1) {
                             ptx::mma_commit2_mc(&bars->kv_empty[slotV], PAIR_MASK);
                             ptx::mma_commit2_mc(&bars->pv_done[t], PAIR_MASK);
                             if (j == n_kv - 1) ptx::mma_commit2_mc(&bars->o_final, PAIR_MASK);
@@ -375,11 +379,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_wait(&bars->s_full[g], (j / NG) & 1);
             ptx::tc_fence_after();
             if (tr) TRACE(j, 4);
-            // pass 1: row max over the 128 keys, two rounds of 64 columns (keeps registers low)
+            // pass 1: row max over the 128 keys, two rounds of 64 columns; the half pass 2 processes first is
+            // read second and its scores stay in registers (ka, kb) for pass 2
             float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+            uint32_t ka[32], kb[32];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                uint32_t sa[32], sb[32];
+            for (int r = 0; r < 2; ++r) {
+                const int h = HALF_ORDER[1 - r];
+                uint32_t ta[32], tb[32];
+                uint32_t (&sa)[32] = r ? ka : ta;
+                uint32_t (&sb)[32] = r ? kb : tb;
                 ptx::tmem_ld32(tS + 64 * h, sa);
                 ptx::tmem_ld32(tS + 64 * h + 32, sb);
                 ptx::tmem_wait_ld();
@@ -444,16 +453,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t NEGM = ptx::f2pack(-m, -m);
             uint64_t L0 = ptx::f2pack(0.f, 0.f), L1 = L0;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                uint32_t sa[32], sb[32];
-                ptx::tmem_ld32(tS + 64 * h, sa);
-                ptx::tmem_ld32(tS + 64 * h + 32, sb);
-                ptx::tmem_wait_ld();
-                if (masked) {
+            for (int o = 0; o < 2; ++o) {
+                const int h = HALF_ORDER[o];
+                uint32_t ta[32], tb[32];
+                uint32_t (&sa)[32] = o ? ta : ka;   // the first half is still in registers (masked in pass 1)
+                uint32_t (&sb)[32] = o ? tb : kb;
+                if (o) {
+                    ptx::tmem_ld32(tS + 64 * h, sa);
+                    ptx::tmem_ld32(tS + 64 * h + 32, sb);
+                    ptx::tmem_wait_ld();
+                    if (masked) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        if (64 * h + i >= last_valid) sa[i] = 0xff800000u;
-                        if (64 * h + 32 + i >= last_valid) sb[i] = 0xff800000u;
+                        for (int i = 0; i < 32; ++i) {
+                            if (64 * h + i >= last_valid) sa[i] = 0xff800000u;
+                            if (64 * h + 32 + i >= last_valid) sb[i] = 0xff800000u;
+                        }
                     }
                 }
                 uint32_t pk[32];
@@ -481,7 +495,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(&bars->p_full[g][h], 0));   // the leader's
-                if (tr && h == 0) TRACE(j, 8);
+                if (tr && o == 0) TRACE(j, 8);
             }
             {
                 float a0, a1, b0, b1;
