@@ -185,6 +185,34 @@ def ring_forward(Qs, Ks, Vs, attn_lse) -> List[np.ndarray]:
     return outs
 
 
+def usp_forward(Qs, Ks, Vs, U: int, attn_lse) -> List[np.ndarray]:
+    """USP hybrid (PAPER.md:171 -- Ulysses degree U x Ring degree R = P/U; R21): ranks
+    [rho*U, rho*U+U) form Ulysses group rho.  1. seq->head all-to-all inside each group; 2. ring attention over
+    the R groups among the ranks with the same position u in their group (heads u*H/U.. of every group's
+    tokens); 3. head->seq all-to-all inside each group."""
+    P = len(Qs)
+    R = P // U
+    heads = [None] * P
+    for t, X in enumerate((Qs, Ks, Vs)):
+        for rho in range(R):
+            hs = seq_to_head(X[rho * U:(rho + 1) * U])            # step 1, group rho
+            for u in range(U):
+                if heads[rho * U + u] is None:
+                    heads[rho * U + u] = [None, None, None]
+                heads[rho * U + u][t] = hs[u]
+    O = [None] * P
+    for u in range(U):                                          # step 2, ring of position u
+        members = [rho * U + u for rho in range(R)]
+        outs = ring_forward([heads[i][0] for i in members], [heads[i][1] for i in members],
+                            [heads[i][2] for i in members], attn_lse)
+        for rho, i in enumerate(members):
+            O[i] = outs[rho]
+    res = []
+    for rho in range(R):                                        # step 3
+        res.extend(head_to_seq(O[rho * U:(rho + 1) * U]))
+    return res
+
+
 # ---------------------------------------------------------------- attention per rank
 def _attn_heads(Rq: np.ndarray, Rk: np.ndarray, Rv: np.ndarray, rows: np.ndarray, heads: Sequence[int],
                 attn: Attn) -> np.ndarray:

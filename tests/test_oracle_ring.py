@@ -70,3 +70,15 @@ def test_ring_equals_unsharded_any_head_count(P, H):
     Q, K, V = (rng.standard_normal((B, S, H, D)) for _ in range(3))
     outs = sp.ring_forward(sp.shard_seq(Q, P), sp.shard_seq(K, P), sp.shard_seq(V, P), oracle.attention_rows_lse)
     np.testing.assert_allclose(np.concatenate(outs, axis=1), oracle.mha_unsharded(Q, K, V), rtol=0, atol=1e-13)
+
+
+@pytest.mark.parametrize("P,U,H", [(4, 2, 2), (4, 2, 6), (6, 3, 3), (8, 4, 4), (4, 4, 4), (4, 1, 3)])
+def test_usp_hybrid_equals_unsharded(P, U, H):
+    """Ulysses degree U x Ring degree P/U = unsharded attention; U = P is plain Ulysses with a
+    single-block ring, U = 1 plain Ring."""
+    rng = np.random.default_rng(P * 100 + U * 10 + H)
+    B, S_l, D = 1, 3, 4
+    S = S_l * P
+    Q, K, V = (rng.standard_normal((B, S, H, D)) for _ in range(3))
+    outs = sp.usp_forward(sp.shard_seq(Q, P), sp.shard_seq(K, P), sp.shard_seq(V, P), U, oracle.attention_rows_lse)
+    np.testing.assert_allclose(np.concatenate(outs, axis=1), oracle.mha_unsharded(Q, K, V), rtol=0, atol=1e-13)
