@@ -99,6 +99,12 @@ typedef struct {
                        Ulysses to Ring-Attention ... avoiding the overhead of padding"; R21): every
                        rank keeps all H heads of its sequence shard, only S % nranks == 0 is required (any H);
                        use spa_ring_attention*.  stages, n_src and pad_heads must be 0 / 1 / 0. */
+    int ulysses;    /* ring plans only: Ulysses degree U of the USP hybrid ("flexible configuration
+                       of both the Ulysses degree and the Ring-Attention degree"); 0 or 1 = pure Ring.  U > 1:
+                       U | nranks and U | H; ranks [rho*U, rho*U+U) form Ulysses group rho, the R = nranks/U
+                       groups form rings (seq->head all-to-all in the group, Ring attention over the groups on
+                       H/U heads, head->seq all-to-all).  NCCL plans split the comm (plan creation is then
+                       collective). */
 } spa_shape;
 
 /* Validates everything synchronously.  Requirements: D in {64,96,128}; S % n_src == 0;

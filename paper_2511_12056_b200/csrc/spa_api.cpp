@@ -94,6 +94,12 @@ struct spa_plan {
     // ring plans (shape.ring = 1; R21): per-rank workspace = 2 K/V receive slots + P fp32 partials + lse
     bool ring = false;
     long long E_loc = 0;                         // B * S_l * H * D
+    // USP hybrid (shape.ring = 1, shape.ulysses = U > 1): Ulysses over groups of U consecutive ranks, Ring over
+    // the R = P/U groups.  Sub-comms / sub-plans owned by this plan; ws = 4 head-sharded tensors + sub-plan ws.
+    int U = 1, R = 1;
+    spa_comm *uly_comm = nullptr, *ring_comm = nullptr;
+    spa_plan *uly_plan = nullptr, *ring_plan = nullptr;
+    long long ws_total = -1;                     // >= 0: spa_plan_workspace_bytes returns this
     long long off_kvbuf = 0, off_parts = 0, off_lse = 0;
     Split split;
     // per-rank workspace layout (bytes)
@@ -589,6 +595,96 @@ int n_local_srcs(const spa_plan *p) { return p->comm->kind == KIND_LOOPBACK ? p-
 
 }  // namespace
 
+// ------------------------------------------------------------------ USP hybrid plan (R21)
+// Ranks p = rho*U + u: Ulysses group rho = ranks [rho*U, rho*U+U), ring index u.  Step 1: seq->head all-to-all
+// inside each group (heads [u*H/U, (u+1)*H/U) of the group's U*S_l tokens on rank (rho, u)); step 2: Ring
+// attention over the R groups among the ranks with the same u; step 3: head->seq all-to-all inside the group.
+static spa_status create_usp_plan(spa_plan **plan, spa_comm *comm, const spa_shape &s) {
+    const int P = comm->nranks, U = s.ulysses;
+    if (P % U) return fail(SPA_ERR_SHAPE, "ulysses degree must divide nranks");
+    if (s.H % U) return fail(SPA_ERR_SHAPE, "H must be divisible by the ulysses degree");
+    if (s.S % P) return fail(SPA_ERR_SHAPE, "S must be divisible by nranks");
+    if (s.n_src != 0 && s.n_src != P) return fail(SPA_ERR_SHAPE, "USP plans have no co-processor ranks");
+    const int R = P / U;
+    spa_plan *p = new spa_plan;
+    p->comm = comm; p->sh = s; p->P = P; p->Psrc = P; p->ring = true; p->U = U; p->R = R;
+    p->Hp = s.H; p->h = s.H; p->S_l = s.S / P;
+    p->split = make_split(1, p->S_l, 1);
+    p->E_loc = (long long)s.B * p->S_l * s.H * s.D;
+    auto cleanup = [&](spa_status st) { spa_plan_destroy(p); return st; };
+    spa_status st = SPA_OK;
+    if (comm->kind == KIND_LOOPBACK) {
+        st = spa_comm_init_loopback(&p->uly_comm, U, comm->device);
+        if (st == SPA_OK) st = spa_comm_init_loopback(&p->ring_comm, R, comm->device);
+    } else if (comm->kind == KIND_HOST) {
+        st = spa_comm_init_host(&p->uly_comm, U, comm->rank % U);
+        if (st == SPA_OK) st = spa_comm_init_host(&p->ring_comm, R, comm->rank / U);
+    } else {
+        st = spa_comm_split(comm, comm->rank / U, comm->rank % U, &p->uly_comm);
+        if (st == SPA_OK) st = spa_comm_split(comm, comm->rank % U, comm->rank / U, &p->ring_comm);
+    }
+    if (st != SPA_OK) return cleanup(st);
+    spa_shape us{s.B, U * p->S_l, s.H, s.D, 1, 0, 0, 0, 0};
+    spa_shape rs{s.B, s.S, s.H / U, s.D, 1, 0, 0, 1, 0};
+    st = spa_plan_create(&p->uly_plan, p->uly_comm, &us);
+    if (st == SPA_OK) st = spa_plan_create(&p->ring_plan, p->ring_comm, &rs);
+    if (st != SPA_OK) return cleanup(st);
+    size_t wu = 0, wr = 0;
+    spa_plan_workspace_bytes(p->uly_plan, &wu);
+    spa_plan_workspace_bytes(p->ring_plan, &wr);
+    const int nloc = comm->kind == KIND_LOOPBACK ? P : 1;
+    p->off_kvbuf = 0;   // head-sharded Q, K, V, O per (local) rank: [nloc][4][E_loc] bf16
+    p->off_parts = align_up((long long)nloc * 4 * p->E_loc * 2, 256);   // sub-plan workspace
+    p->ws_total = p->off_parts + (long long)std::max(wu, wr);
+    *plan = p;
+    return SPA_OK;
+}
+
+static spa_status usp_call(spa_plan *p, const void *const q[], const void *const k[], const void *const v[],
+                           void *const out[], void *ws, void *stream, bool local) {
+    if (p->comm->kind == KIND_HOST) return fail(SPA_ERR_UNSUPPORTED, "host-only comm cannot execute");
+    if (local != (p->comm->kind == KIND_LOOPBACK))
+        return fail(SPA_ERR_INVALID, local ? "*_local calls need a loopback plan" : "loopback plans need the *_local calls");
+    SPA_TRY(check_ptr(ws, "ws"));
+    const int U = p->U, R = p->R, nloc = local ? p->P : 1;
+    for (int i = 0; i < nloc; ++i) {
+        SPA_TRY(check_ptr(q[i], "q")); SPA_TRY(check_ptr(k[i], "k"));
+        SPA_TRY(check_ptr(v[i], "v")); SPA_TRY(check_ptr(out[i], "out"));
+    }
+    uint8_t *w = reinterpret_cast<uint8_t *>(ws);
+    uint8_t *sub_ws = w + p->off_parts;
+    auto head = [&](int i, int t) { return w + ((long long)i * 4 + t) * p->E_loc * 2; };   // t: 0 Q 1 K 2 V 3 O
+    const void *const *in[3] = {q, k, v};
+    if (!local) {
+        for (int t = 0; t < 3; ++t) SPA_TRY(spa_reshard_seq_to_head(p->uly_plan, in[t][0], head(0, t), sub_ws, stream));
+        SPA_TRY(spa_ring_attention(p->ring_plan, head(0, 0), head(0, 1), head(0, 2), head(0, 3), sub_ws, stream));
+        return spa_reshard_head_to_seq(p->uly_plan, head(0, 3), out[0], sub_ws, stream);
+    }
+    std::vector<const void *> xs(U);
+    std::vector<void *> hs(U);
+    for (int rho = 0; rho < R; ++rho)   // step 1 per Ulysses group
+        for (int t = 0; t < 3; ++t) {
+            for (int u = 0; u < U; ++u) { xs[u] = in[t][rho * U + u]; hs[u] = head(rho * U + u, t); }
+            SPA_TRY(spa_reshard_seq_to_head_local(p->uly_plan, xs.data(), hs.data(), sub_ws, stream));
+        }
+    std::vector<const void *> rq(R), rk(R), rv(R);
+    std::vector<void *> ro(R);
+    for (int u = 0; u < U; ++u) {   // step 2 per ring
+        for (int rho = 0; rho < R; ++rho) {
+            const int i = rho * U + u;
+            rq[rho] = head(i, 0); rk[rho] = head(i, 1); rv[rho] = head(i, 2); ro[rho] = head(i, 3);
+        }
+        SPA_TRY(spa_ring_attention_local(p->ring_plan, rq.data(), rk.data(), rv.data(), ro.data(), sub_ws, stream));
+    }
+    std::vector<void *> os(U);
+    for (int rho = 0; rho < R; ++rho) {   // step 3 per Ulysses group
+        for (int u = 0; u < U; ++u) { hs[u] = head(rho * U + u, 3); os[u] = out[rho * U + u]; }
+        std::vector<const void *> hc(hs.begin(), hs.end());
+        SPA_TRY(spa_reshard_head_to_seq_local(p->uly_plan, hc.data(), os.data(), sub_ws, stream));
+    }
+    return SPA_OK;
+}
+
 // ==================================================================== C ABI
 extern "C" {
 
@@ -720,6 +816,8 @@ spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *sha
     if (s.S % Psrc) return fail(SPA_ERR_SHAPE, "S must be divisible by the number of source ranks");
     if (s.pad_heads != 0 && s.pad_heads != 1) return fail(SPA_ERR_INVALID, "pad_heads must be 0 or 1");
     if (s.ring != 0 && s.ring != 1) return fail(SPA_ERR_INVALID, "ring must be 0 or 1");
+    if (s.ulysses < 0 || (!s.ring && s.ulysses > 1)) return fail(SPA_ERR_INVALID, "ulysses degree needs ring = 1");
+    if (s.ring && s.ulysses > 1) return create_usp_plan(plan, comm, s);
     if (s.ring) {
         // Ring attention: every rank keeps all heads; only S % P matters.
         if (s.n_src != 0 && s.n_src != P) return fail(SPA_ERR_SHAPE, "ring plans have no co-processor ranks");
@@ -768,6 +866,10 @@ spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *sha
 
 spa_status spa_plan_workspace_bytes(const spa_plan *plan, size_t *bytes) {
     if (!plan || !bytes) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (plan->ws_total >= 0) {
+        *bytes = (size_t)plan->ws_total;
+        return SPA_OK;
+    }
     long long per = plan->ws_rank_bytes;
     *bytes = (size_t)(plan->comm->kind == KIND_LOOPBACK ? per * plan->P : per);
     return SPA_OK;
@@ -783,6 +885,10 @@ spa_status spa_plan_stage_split(const spa_plan *plan, int *G_h, int *C, int *g) 
 
 spa_status spa_plan_destroy(spa_plan *plan) {
     if (!plan) return SPA_OK;
+    spa_plan_destroy(plan->uly_plan);
+    spa_plan_destroy(plan->ring_plan);
+    if (plan->uly_comm) spa_comm_destroy(plan->uly_comm);
+    if (plan->ring_comm) spa_comm_destroy(plan->ring_comm);
     for (auto e : plan->sync_ev) cudaEventDestroy(e);
     for (auto e : plan->prof_ev) cudaEventDestroy(e);
     if (plan->sc_alt) cudaStreamDestroy(plan->sc_alt);
@@ -901,6 +1007,7 @@ static spa_status ring_call(spa_plan *p, int n, const void *const q[], const voi
     if (!p) return fail(SPA_ERR_INVALID, "plan is NULL");
     if (!p->ring) return fail(SPA_ERR_INVALID, "not a ring plan (shape.ring = 1)");
     if (p->kv_len) return fail(SPA_ERR_UNSUPPORTED, "key-padding masks are not supported on ring plans");
+    if (p->U > 1) return usp_call(p, q, k, v, out, ws, stream, local);
     Exec x{};
     SPA_TRY(prepare(p, x, ws, stream, local));
     for (int i = 0; i < n; ++i) {

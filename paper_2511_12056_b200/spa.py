@@ -37,7 +37,7 @@ class SpaError(RuntimeError):
 class Shape(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int), ("S", ctypes.c_int), ("H", ctypes.c_int), ("D", ctypes.c_int),
                 ("stages", ctypes.c_int), ("n_src", ctypes.c_int), ("pad_heads", ctypes.c_int),
-                ("ring", ctypes.c_int)]
+                ("ring", ctypes.c_int), ("ulysses", ctypes.c_int)]
 
 
 class Profile(ctypes.Structure):
@@ -230,9 +230,9 @@ class Comm:
 
 class Plan:
     def __init__(self, comm: Comm, B: int, S: int, H: int, D: int, stages: int = 1, n_src: int = 0,
-                 pad_heads: bool = False, ring: bool = False):
+                 pad_heads: bool = False, ring: bool = False, ulysses: int = 0):
         self.comm = comm
-        self.shape = Shape(B, S, H, D, stages, n_src, int(bool(pad_heads)), int(bool(ring)))
+        self.shape = Shape(B, S, H, D, stages, n_src, int(bool(pad_heads)), int(bool(ring)), int(ulysses))
         h = ctypes.c_void_p()
         _check(load().spa_plan_create(ctypes.byref(h), comm.h, ctypes.byref(self.shape)), "spa_plan_create")
         self.h = h

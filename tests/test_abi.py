@@ -92,6 +92,20 @@ def test_ring_plan_validation_and_workspace():
     assert spa.Plan(spa.Comm.host(1, 0), B, S, H, D, ring=True).workspace_bytes == 0
 
 
+def test_usp_plan_validation():
+    """USP hybrid: Ulysses degree U | nranks and U | H; sub-plans on sub-comms."""
+    p = spa.Plan(spa.Comm.host(8, 3), 1, 8 * 64, 12, 128, ring=True, ulysses=4)
+    assert p.workspace_bytes > 4 * 64 * 12 * 128 * 2
+    for kw, err in [(dict(ulysses=3), 2), (dict(ulysses=8, H=12), 2)]:
+        H = kw.pop("H", 12)
+        with pytest.raises(spa.SpaError) as e:
+            spa.Plan(spa.Comm.host(8, 0), 1, 8 * 64, H, 128, ring=True, **kw)
+        assert e.value.status == err
+    with pytest.raises(spa.SpaError) as e:
+        spa.Plan(spa.Comm.host(8, 0), 1, 8 * 64, 12, 128, ulysses=4)   # needs ring = 1
+    assert e.value.status == 1
+
+
 def test_host_comm_cannot_execute():
     comm = spa.Comm.host(2, 1)
     plan = spa.Plan(comm, 1, 256, 4, 64, stages=2)

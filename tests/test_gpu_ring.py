@@ -53,3 +53,26 @@ def test_ring_closed_forms():
     assert (out - mean).abs().max().item() < 2e-3
     q, k, v = U.qkv(B, S, H, D, dist="D3")   # V = 1 -> 1
     assert (_ring(P, q, k, v).double().cpu() - 1).abs().max().item() <= 2 ** -7
+
+
+def _usp(P, U, q, k, v):
+    B, S, H, D = q.shape
+    plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, ring=True, ulysses=U)
+    qs, ks, vs = _shards(q, P), _shards(k, P), _shards(v, P)
+    outs = [torch.full_like(t, float("nan")) for t in qs]
+    ws = plan.workspace()
+    spa.spa_ring_attention_local(plan, qs, ks, vs, outs, ws)
+    torch.cuda.synchronize()
+    return torch.cat(outs, dim=1)
+
+
+@pytest.mark.parametrize("P,Ud,H,D", [(4, 2, 6, 128), (8, 2, 6, 96), (8, 4, 12, 64), (6, 3, 9, 128)])
+def test_usp_hybrid_vs_oracle(P, Ud, H, D):
+    """USP (Ulysses degree U x Ring degree P/U) through the C ABI: reshards inside Ulysses groups,
+    ring attention across them; within tolerance of the oracle and deterministic."""
+    B, S = 1, 64 * P
+    q, k, v = U.qkv(B, S, H, D, seed=P * 10 + Ud)
+    out = _usp(P, Ud, q, k, v)
+    assert not torch.isnan(out).any()
+    U.assert_close(out, U.oracle_mha(q, k, v))
+    assert torch.equal(out.view(torch.int16), _usp(P, Ud, q, k, v).view(torch.int16))
