@@ -52,18 +52,7 @@ namespace spa {
 namespace {
 
 constexpr int BM = 128;        // query rows per CTA (MMA M)
-constexpr int BN = 128;        // keys per tile (MMA N of QK^T, K of PV)
-constexpr int NG = 3;          // softmax groups = S buffers in TMEM = independent S->softmax->PV chains
-constexpr int NUM_SOFTMAX_WARPS = 4 * NG;
-// Four warpgroups: three of softmax warps, then {producer, 2 idle, MMA}.  The last warpgroup gives its
-// registers to the softmax warps (setmaxnreg): per SM sub-partition 3 x 152 + 56 = 512 registers per lane.
-constexpr int PRODUCER_WARP = NUM_SOFTMAX_WARPS;
-// The MMA issuer has the highest warp id: the warp scheduler favours higher ids, and its few instructions
-// must not queue behind the softmax warps that share its SM sub-partition.
-constexpr int MMA_WARP = NUM_SOFTMAX_WARPS + 3;
-constexpr int NUM_WARPS = NUM_SOFTMAX_WARPS + 4;
-constexpr int NUM_THREADS = NUM_WARPS * 32;
-constexpr int SOFTMAX_REGS = 152, AUX_REGS = 56;
+constexpr int NG_MAX = 4;
 constexpr float RESCALE_TAU = 8.0f;   // log2 domain: raise the running max only if it grows by > 2^8
 // CTA pair: clusters of 2 adjacent query tiles of one head run every MMA as ONE cta_group::2 instruction
 // (M = 256); each CTA holds only half of every K tile (64 keys) and half of every V tile (D/2 columns), so
@@ -72,10 +61,8 @@ constexpr uint16_t PAIR_MASK = 0x3;
 // Order in which the softmax releases (and the MMA consumes) the two 64-key halves of P: the upper half first,
 // straight from the registers pass 1 loaded last (one TMEM read of 64 columns per tile saved).
 __device__ constexpr int HALF_ORDER[2] = {1, 0};
-// named barriers: 0 = __syncthreads; 1 + 3*wq + g = "running max of the previous tile is in xm[] for the
-// warp of group g on lane quarter wq"; 1 + 3*4 = all softmax warps (epilogue merge).
-constexpr uint32_t BAR_EPI = 1 + 3 * 4;
-static_assert(NG == 3, "barrier numbering assumes three groups");
+
+
 
 #ifdef SPA_ATTN_TRACE
 // Debug timeline of CTA (0,0,0): g_trace[j][e] = clock64 at event e of KV iteration j (tools/attn_trace.py).
@@ -85,13 +72,51 @@ __device__ unsigned long long g_trace[256][16];
         if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 256)      \
             g_trace[(j)][(e)] = clock64();                                           \
     } while (0)
+// per softmax warp of both CTAs of cluster 0: [j][crank*4 + wq][0] = S(j) seen, [1] = first P half released,
+// [2] = second P half released (clock64 of that SM)
+__device__ unsigned long long g_trace2[256][8][3];
+#define TRACE2(j, slot, e)                                                                     \
+    do {                                                                                      \
+        if (blockIdx.x < 2 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 256 && lane == 0)    \
+            g_trace2[(j)][(slot)][(e)] = clock64();                                           \
+    } while (0)
 #else
 #define TRACE(j, e) do {} while (0)
+#define TRACE2(j, slot, e) do {} while (0)
 #endif
 
 template <int D>
 struct Cfg {
     static_assert(D == 64 || D == 96 || D == 128, "D in {64, 96, 128}");
+    // Keys per KV tile (MMA N of QK^T, K of PV) and softmax groups = S buffers in TMEM = independent
+    // S -> softmax -> PV chains: three chains of 128-key tiles.  SPA_NG4_D96 builds D=96 with four chains of
+    // 96-key tiles (4 x 96 + 96 = 480 TMEM columns, 104 softmax registers); measured 1-3 % slower
+    // (profiles/r01_v5_experiments/README.md), so it is not the default.
+#ifdef SPA_NG4_D96
+    static constexpr int BN = (D == 96) ? 96 : 128;
+    static constexpr int NG = (D == 96) ? 4 : 3;
+#else
+    static constexpr int BN = 128;
+    static constexpr int NG = 3;
+#endif
+    static constexpr int HALF = BN / 2;                  // keys per P release (64 or 48)
+    static constexpr int NUM_SOFTMAX_WARPS = 4 * NG;
+    // NG warpgroups of softmax warps, then {producer, 2 idle, MMA}.  The last warpgroup gives its registers to
+    // the softmax warps (setmaxnreg): per SM sub-partition NG x SOFTMAX_REGS + AUX_REGS <= (NG + 1) x LAUNCH_REGS.
+    static constexpr int PRODUCER_WARP = NUM_SOFTMAX_WARPS;
+    // The MMA issuer has the highest warp id: the warp scheduler favours higher ids, and its few instructions
+    // must not queue behind the softmax warps that share its SM sub-partition.
+    static constexpr int MMA_WARP = NUM_SOFTMAX_WARPS + 3;
+    static constexpr int NUM_THREADS = (NUM_SOFTMAX_WARPS + 4) * 32;
+    // setmaxnreg only moves registers within the CTA's launch allocation (65536 / NUM_THREADS rounded down to
+    // a multiple of 8 per thread: 128 for 512 threads, 96 for 640), so the split must fit that pool.
+    static constexpr int LAUNCH_REGS = (65536 / NUM_THREADS) / 8 * 8;
+    static constexpr int SOFTMAX_REGS = (NG == 4) ? 104 : 152, AUX_REGS = (NG == 4) ? 64 : 56;
+    static_assert(NG * SOFTMAX_REGS + AUX_REGS <= (NG + 1) * LAUNCH_REGS, "register split exceeds the CTA pool");
+    // Named barriers (0 = __syncthreads).  NG = 3: 1 + 3*wq + g = "running max of the previous tile is in xm[]
+    // for the warp of group g on lane quarter wq" (64 threads); NG = 4 (16 would not fit): 1 + g for the four
+    // warps of group g and of the group before it (256 threads).  BAR_EPI: all softmax warps (epilogue merge).
+    static constexpr uint32_t BAR_EPI = (NG == 3) ? 13 : 5;
     // Q/K tiles (K-major operands): 64-column 128B-swizzled chunks + (D=96) one 32-column 64B-swizzled chunk.
     static constexpr int N128 = D / 64;                  // 1, 1, 2
     static constexpr int N64 = (D % 64) ? 1 : 0;         // 0, 1, 0
@@ -103,17 +128,18 @@ struct Cfg {
     static constexpr int V_ATOM_COLS = (D == 128) ? 64 : (D == 64 ? 32 : 16);
     static constexpr uint32_t V_LAYOUT = (D == 128) ? 2u : (D == 64 ? 4u : 6u);   // SW128 / SW64 / SW32
     static constexpr int V_ATOMS = VH / V_ATOM_COLS;
-    static constexpr int V_ATOM_BYTES = BM * V_ATOM_COLS * 2;
-    static constexpr int TILE_BYTES = BM * D * 2;        // Q tile; a whole K or V tile of the pair
-    static constexpr int HALF_BYTES = TILE_BYTES / 2;    // one ring slot: this CTA's half of a K or V tile
-    static constexpr int KCHUNK = (BN / 2) * 128;        // K half: 64 keys; 64-column SW128 chunk c at c*KCHUNK
+    static constexpr int V_ATOM_BYTES = BN * V_ATOM_COLS * 2;
+    static constexpr int TILE_BYTES = BM * D * 2;        // Q tile
+    static constexpr int KV_TILE_BYTES = BN * D * 2;     // a whole K or V tile of the pair
+    static constexpr int HALF_BYTES = KV_TILE_BYTES / 2; // one ring slot: this CTA's half of a K or V tile
+    static constexpr int KCHUNK = (BN / 2) * 128;        // K half: BN/2 keys; 64-column SW128 chunk c at c*KCHUNK
     // K/V ring slots (as many as fit: the ring depth is the TMA lookahead that hides L2 latency)
     static constexpr int NS = (D == 128) ? 12 : 16;
     static constexpr int BAR_BYTES = 512;
     static constexpr int XCH_BYTES = BM * 4;   // static smem: running max (the epilogue's (m, l) reuse ring slot 0)
     static constexpr int SMEM_BYTES = 1024 /*align slack*/ + TILE_BYTES + NS * HALF_BYTES + BAR_BYTES;
     static constexpr uint32_t TMEM_COLS = 512;
-    static constexpr uint32_t O_COL = 128 * NG;          // O accumulator columns [O_COL, O_COL + D)
+    static constexpr uint32_t O_COL = BN * NG;           // O accumulator columns [O_COL, O_COL + D)
     static_assert(O_COL + D <= TMEM_COLS, "TMEM budget");
     static constexpr int OCHUNKS = D / 16;               // epilogue: 16-column chunks, chunk c by group c % NG
     // exp2 split: key pairs with (key & 15) >= POLY_FROM use the FMA-pipe polynomial, the rest MUFU.EX2
@@ -134,9 +160,9 @@ struct SmemBars {
     uint64_t q_full;
     uint64_t kv_full[16];      // leader's count the data of both CTAs' halves (follower's unused)
     uint64_t kv_empty[16];
-    uint64_t s_full[NG];       // [buffer]: S(j) complete
-    uint64_t p_full[NG][2];    // [buffer][key half]: P(j) half written (leader's: 4 warps of the group in each CTA)
-    uint64_t pv_done[NG];      // [buffer]: PV(j) complete (O may be rescaled)
+    uint64_t s_full[NG_MAX];       // [buffer]: S(j) complete
+    uint64_t p_full[NG_MAX][2];    // [buffer][key half]: P(j) half written (leader's: 4 warps of the group, both CTAs)
+    uint64_t pv_done[NG_MAX];      // [buffer]: PV(j) complete (O may be rescaled)
     uint64_t o_final;          // all PVs completed (epilogue)
     uint32_t tmem_base;
 };
@@ -164,12 +190,14 @@ __device__ __forceinline__ void ex2_poly2(uint64_t X, float &y0, float &y1) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQa, const __grid_constant__ CUtensorMap tmQb,
                     const __grid_constant__ CUtensorMap tmKa, const __grid_constant__ CUtensorMap tmKb,
                     const __grid_constant__ CUtensorMap tmVa, const __grid_constant__ CUtensorMap tmVb,
                     const AttnArgs args) {
     using C = Cfg<D>;
+    constexpr int BN = C::BN, NG = C::NG, HALF = C::HALF;
+    constexpr int NUM_SOFTMAX_WARPS = C::NUM_SOFTMAX_WARPS, PRODUCER_WARP = C::PRODUCER_WARP, MMA_WARP = C::MMA_WARP;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sQ = smem;                                        // this CTA's Q tile
@@ -226,7 +254,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     if (warp == PRODUCER_WARP) {
         // ------------------------------------------------------------ TMA producer
-        ptx::setmaxnreg_dec<AUX_REGS>();
+        ptx::setmaxnreg_dec<C::AUX_REGS>();
         const uint64_t pol_q = ptx::policy_evict_first();
         const uint64_t pol_kv = ptx::policy_evict_last();
         // Every load of either CTA is counted on the LEADER's barrier, which expects the pair's bytes.
@@ -238,7 +266,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (C::N64) ptx::tma_load_4d_2sm(&tmQb, qbar, sQ + chunk_off(1), 64, head, qtile * BM, b, pol_q);
         }
         int cnt = 0;
-        // K half: keys [j*128 + 64*crank, +64) of tile j, all D columns; V half: all 128 keys, columns
+        // K half: keys [j*BN + crank*BN/2, +BN/2) of tile j, all D columns; V half: all BN keys, columns
         // [crank*D/2, +D/2).  A slot is refilled once the pair's MMA that read it completed (kv_empty).
         auto load = [&](bool isV, int j) {
             const int slot = cnt % C::NS;
@@ -246,7 +274,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (lane == 0) {
                 uint8_t *dst = sKV + slot * C::HALF_BYTES;
                 const uint32_t bar = ptx::mapa(&bars->kv_full[slot], 0);
-                if (crank == 0) ptx::mbar_arrive_expect_tx(&bars->kv_full[slot], C::TILE_BYTES);
+                if (crank == 0) ptx::mbar_arrive_expect_tx(&bars->kv_full[slot], C::KV_TILE_BYTES);
                 auto tl = [&](const CUtensorMap *m, uint8_t *d, int c0, int row) {
                     ptx::tma_load_4d_2sm(m, bar, d, c0, head, row, b, pol_kv);
                 };
@@ -273,7 +301,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp == MMA_WARP) {
         // ------------------------------------------------------------ MMA issuer
-        ptx::setmaxnreg_dec<AUX_REGS>();
+        ptx::setmaxnreg_dec<C::AUX_REGS>();
         constexpr uint32_t IDESC_QK = ptx::idesc_bf16(2 * BM, BN, 0, 0);   // the pair: M = 256
         constexpr uint32_t IDESC_PV = ptx::idesc_bf16(2 * BM, D, 0, 1);
         const uint32_t qa = ptx::smem_u32(sQ);
@@ -302,7 +330,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (leader) {
                 TRACE(j, 2);
                 const uint64_t so = (uint64_t)(slot * C::HALF_BYTES) >> 4;
-                const uint32_t d = tmem + (j % NG) * 128;
+                const uint32_t d = tmem + (j % NG) * BN;
 #pragma unroll
                 for (int c = 0; c < C::NCHUNK; ++c) {
                     const bool sw64 = (c >= C::N128);
@@ -326,7 +354,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int j = 0; j < NG && j < n_kv; ++j) issue_qk(j);
             for (int j = 0; j < n_kv; ++j) {
                 const int t = j % NG;
-                const uint32_t tS = tmem + t * 128;
+                const uint32_t tS = tmem + t * BN;
                 const int slotV = acquire();
                 if (leader) TRACE(j, 10);
                 const uint64_t dVs = dV + ((uint64_t)(slotV * C::HALF_BYTES) >> 4);
@@ -337,11 +365,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     ptx::tc_fence_after();
                     if (leader) {
                         TRACE(j, o);
-                        // O (+)= P(j)[keys 64hf..64hf+63] V_j[those keys]; that P half sits in columns 64hf..64hf+31
+                        // O (+)= P(j)[keys HALF*hf ..+HALF) V_j[those keys]; that P half (bf16 pairs) sits in columns
+                        // HALF*hf .. HALF*hf + HALF/2 of the S buffer
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            const int key16 = hf * 4 + kk;
-                            ptx::mma_ts2(tO, tS + hf * 64 + kk * 8, dVs + ((uint64_t)(key16 * 16 * rowb) >> 4),
+                        for (int kk = 0; kk < HALF / 16; ++kk) {
+                            const int key16 = hf * (HALF / 16) + kk;
+                            ptx::mma_ts2(tO, tS + hf * HALF + kk * 8, dVs + ((uint64_t)(key16 * 16 * rowb) >> 4),
                                          IDESC_PV, (j > 0 || o > 0 || kk > 0) ? 1u : 0u);
                         }
                         if (o == 1) {
@@ -357,19 +386,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp < NUM_SOFTMAX_WARPS) {
         // ------------------------------------------------------------ softmax / correction / epilogue
-        ptx::setmaxnreg_inc<SOFTMAX_REGS>();
+        ptx::setmaxnreg_inc<C::SOFTMAX_REGS>();
         const int g = warp >> 2;                       // softmax group: KV tiles j with j % NG == g
         const int wq = warp & 3;                       // TMEM lane quarter this warp may access (= SMSP)
         const int row = wq * 32 + lane;                // row within the tile
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-        const uint32_t tS = tmem + lane_base + g * 128;
+        const uint32_t tS = tmem + lane_base + g * BN;
         const uint32_t tO = tmem + lane_base + C::O_COL;
         const float sl2 = args.scale_log2;
         const uint64_t SL2 = ptx::f2pack(sl2, sl2);
-        const int last_valid = Skv_b - (n_kv - 1) * BN;   // valid keys in the last tile (1..128)
+        const int last_valid = Skv_b - (n_kv - 1) * BN;   // valid keys in the last tile (1..BN)
         const bool tr = (lane == 0 && wq == 0);
-        const uint32_t bar_in = 1 + 3 * wq + g;                  // "m of tile j-1 is in xm[]" for this warp
-        const uint32_t bar_out = 1 + 3 * wq + (g + 1) % NG;      // ... for the warp of the next group
+        // "m of tile j-1 is in xm[]" for this warp / for the warp(s) of the next group (see Cfg::BAR_EPI)
+        const uint32_t bar_in = NG == 3 ? 1 + 3 * wq + g : 1 + g;
+        const uint32_t bar_out = NG == 3 ? 1 + 3 * wq + (g + 1) % NG : 1 + (g + 1) % NG;
+        constexpr uint32_t BAR_N = NG == 3 ? 64 : 256;
 
         float mg = -INFINITY;  // the running max this group last used (its l is relative to it)
         float l = 0.f;         // this group's partial row sum (fp32)
@@ -379,32 +410,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_wait(&bars->s_full[g], (j / NG) & 1);
             ptx::tc_fence_after();
             if (tr) TRACE(j, 4);
-            // pass 1: row max over the 128 keys, two rounds of 64 columns; the half pass 2 processes first is
-            // read second and its scores stay in registers (ka, kb) for pass 2
+            TRACE2(j, crank * 4 + wq, 0);
+            // pass 1: row max over the BN keys, two rounds of HALF columns; with 152 registers (NG = 3) the half
+            // pass 2 processes first is read second and its scores stay in registers (kv) for pass 2
+            constexpr bool KEEP = NG == 3;
             float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
-            uint32_t ka[32], kb[32];
+            uint32_t kv[HALF];
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int h = HALF_ORDER[1 - r];
-                uint32_t ta[32], tb[32];
-                uint32_t (&sa)[32] = r ? ka : ta;
-                uint32_t (&sb)[32] = r ? kb : tb;
-                ptx::tmem_ld32(tS + 64 * h, sa);
-                ptx::tmem_ld32(tS + 64 * h + 32, sb);
+                uint32_t tv[HALF];
+                uint32_t (&sv)[HALF] = (r && KEEP) ? kv : tv;
+                ptx::tmem_ld_cols<HALF>(tS + HALF * h, sv);
                 ptx::tmem_wait_ld();
                 if (masked) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        if (64 * h + i >= last_valid) sa[i] = 0xff800000u;
-                        if (64 * h + 32 + i >= last_valid) sb[i] = 0xff800000u;
-                    }
+                    for (int i = 0; i < HALF; ++i)
+                        if (HALF * h + i >= last_valid) sv[i] = 0xff800000u;
                 }
 #pragma unroll
-                for (int i = 0; i < 32; i += 4) {   // FMNMX3: two new scores per instruction, four chains
-                    m0 = ptx::fmax3(m0, __uint_as_float(sa[i]), __uint_as_float(sa[i + 1]));
-                    m1 = ptx::fmax3(m1, __uint_as_float(sa[i + 2]), __uint_as_float(sa[i + 3]));
-                    m2 = ptx::fmax3(m2, __uint_as_float(sb[i]), __uint_as_float(sb[i + 1]));
-                    m3 = ptx::fmax3(m3, __uint_as_float(sb[i + 2]), __uint_as_float(sb[i + 3]));
+                for (int i = 0; i < HALF; i += 8) {   // FMNMX3: two new scores per instruction, four chains
+                    m0 = ptx::fmax3(m0, __uint_as_float(sv[i]), __uint_as_float(sv[i + 1]));
+                    m1 = ptx::fmax3(m1, __uint_as_float(sv[i + 2]), __uint_as_float(sv[i + 3]));
+                    m2 = ptx::fmax3(m2, __uint_as_float(sv[i + 4]), __uint_as_float(sv[i + 5]));
+                    m3 = ptx::fmax3(m3, __uint_as_float(sv[i + 6]), __uint_as_float(sv[i + 7]));
                 }
             }
             const float mx = ptx::fmax3(m0, m1, fmaxf(m2, m3)) * sl2;
@@ -412,7 +441,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // running max after tile j-1, handed over by the previous group (strict tile order)
             float mprev = -INFINITY;
             if (j > 0) {
-                ptx::named_bar_sync(bar_in, 64);
+                ptx::named_bar_sync(bar_in, BAR_N);
                 mprev = xm[row];
             }
             const bool resc = mx > mprev + RESCALE_TAU;   // also true on tile 0 (mprev = -inf)
@@ -420,7 +449,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (j + 1 < n_kv) {
                 xm[row] = m;
                 __threadfence_block();
-                ptx::named_bar_arrive(bar_out, 64);
+                ptx::named_bar_arrive(bar_out, BAR_N);
             }
             if (tr) TRACE(j, 5);
             if (m != mg) {   // this group's partial sum follows the reference max
@@ -431,9 +460,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 // O *= 2^(mprev - m) for the moved rows (others by exactly 1), after PV(j-1), the last product
                 // into O, completed; PV(j) waits for this P.
                 const float factor = resc ? ptx::ex2(mprev - m) : 1.f;
-                // PV(j-1) is completion jp/NG of pv_done[jp%NG].  The parity test is unambiguous: PV(j-4) was
+                // PV(j-1) is completion jp/NG of pv_done[jp%NG].  The parity test is unambiguous: PV(j-1-NG) was
                 // committed before S(j-1), which the previous group saw complete before handing over the max,
-                // and PV(j+2) cannot complete before PV(j), which needs this group's P(j).
+                // and PV(j-1+NG) cannot complete before PV(j), which needs this group's P(j).
                 const int jp = j - 1;
                 ptx::mbar_wait(&bars->pv_done[jp % NG], (jp / NG) & 1);
                 ptx::tc_fence_after();
@@ -447,36 +476,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     ptx::tmem_st32(tO + 32 * c, r);
                 }
             }
-            // pass 2, per 64-key half: reload the scores, P = exp2(s*sl2 - m) in f32x2 pairs (MUFU or FMA-pipe
-            // polynomial by column), bf16 pairs written over the half's first 32 score columns (already read),
-            // released to the MMA issuer.
+            // pass 2, per HALF-key half: P = exp2(s*sl2 - m) in f32x2 pairs (MUFU or FMA-pipe polynomial by
+            // column), bf16 pairs written over the half's first HALF/2 score columns (already read), released to
+            // the MMA issuer.
             const uint64_t NEGM = ptx::f2pack(-m, -m);
             uint64_t L0 = ptx::f2pack(0.f, 0.f), L1 = L0;
 #pragma unroll
             for (int o = 0; o < 2; ++o) {
                 const int h = HALF_ORDER[o];
-                uint32_t ta[32], tb[32];
-                uint32_t (&sa)[32] = o ? ta : ka;   // the first half is still in registers (masked in pass 1)
-                uint32_t (&sb)[32] = o ? tb : kb;
-                if (o) {
-                    ptx::tmem_ld32(tS + 64 * h, sa);
-                    ptx::tmem_ld32(tS + 64 * h + 32, sb);
+                uint32_t tv[HALF];
+                uint32_t (&sv)[HALF] = (o || !KEEP) ? tv : kv;   // KEEP: the first half is still in registers
+                if (o || !KEEP) {
+                    ptx::tmem_ld_cols<HALF>(tS + HALF * h, sv);
                     ptx::tmem_wait_ld();
                     if (masked) {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            if (64 * h + i >= last_valid) sa[i] = 0xff800000u;
-                            if (64 * h + 32 + i >= last_valid) sb[i] = 0xff800000u;
-                        }
+                        for (int i = 0; i < HALF; ++i)
+                            if (HALF * h + i >= last_valid) sv[i] = 0xff800000u;
                     }
                 }
-                uint32_t pk[32];
+                uint32_t pk[HALF / 2];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
+                for (int i = 0; i < HALF / 2; ++i) {
                     const int e = 2 * i;
-                    const uint32_t u0 = e < 32 ? sa[e] : sb[e - 32];
-                    const uint32_t u1 = e + 1 < 32 ? sa[e + 1] : sb[e + 1 - 32];
-                    const uint64_t X = ptx::ffma2(ptx::f2pack(__uint_as_float(u0), __uint_as_float(u1)), SL2, NEGM);
+                    const uint64_t X =
+                        ptx::ffma2(ptx::f2pack(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])), SL2, NEGM);
                     float p0, p1;
                     if ((e & 15) >= C::POLY_FROM) {
                         ex2_poly2(X, p0, p1);
@@ -490,12 +514,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     else L0 = ptx::fadd2(L0, ptx::f2pack(p0, p1));
                     pk[i] = ptx::pack_bf16x2(p0, p1);
                 }
-                ptx::tmem_st32(tS + 64 * h, pk);
+                ptx::tmem_st_cols<HALF / 2>(tS + HALF * h, pk);
                 ptx::tmem_wait_st();
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(&bars->p_full[g][h], 0));   // the leader's
                 if (tr && o == 0) TRACE(j, 8);
+                TRACE2(j, crank * 4 + wq, 1 + o);
             }
             {
                 float a0, a1, b0, b1;
@@ -512,7 +537,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         xml[g][row] = mg;
         xml[NG + g][row] = l;
-        ptx::named_bar_sync(BAR_EPI, 32 * NUM_SOFTMAX_WARPS);
+        ptx::named_bar_sync(C::BAR_EPI, 32 * NUM_SOFTMAX_WARPS);
         float mm = -INFINITY;
 #pragma unroll
         for (int q = 0; q < NG; ++q) mm = fmaxf(mm, xml[q][row]);   // = the max after the last tile, O's reference
@@ -565,7 +590,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
         }
     } else {
-        ptx::setmaxnreg_dec<AUX_REGS>();   // idle warps of the last warpgroup
+        ptx::setmaxnreg_dec<C::AUX_REGS>();   // idle warps of the last warpgroup
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -620,12 +645,12 @@ cudaError_t launch_d(const AttnProblem &p, cudaStream_t st) {
     CUtensorMap m[6];
     const int vswz = C::V_ATOM_COLS * 2;
     bool ok = make_map(&m[0], p.q, D, p.n_heads, p.Sq, p.B, p.q_tok_stride, p.q_batch_stride, 64, 128) &&
-              make_map(&m[2], p.k, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, 64, 128, BN / 2) &&
+              make_map(&m[2], p.k, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, 64, 128, C::BN / 2) &&
               make_map(&m[4], p.v, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, C::V_ATOM_COLS, vswz,
-                       BN);
+                       C::BN);
     if (ok && C::N64)
         ok = make_map(&m[1], p.q, D, p.n_heads, p.Sq, p.B, p.q_tok_stride, p.q_batch_stride, 32, 64) &&
-             make_map(&m[3], p.k, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, 32, 64, BN / 2);
+             make_map(&m[3], p.k, D, p.n_heads, p.Skv, p.B, p.kv_tok_stride, p.kv_batch_stride, 32, 64, C::BN / 2);
     else {
         m[1] = m[0];
         m[3] = m[2];
@@ -655,7 +680,7 @@ cudaError_t launch_d(const AttnProblem &p, cudaStream_t st) {
     const int qtiles = (p.Sq + BM - 1) / BM;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((qtiles + 1) / 2 * 2, p.n_heads, p.B);
-    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.blockDim = dim3(C::NUM_THREADS);
     cfg.dynamicSmemBytes = C::SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -673,6 +698,9 @@ cudaError_t launch_d(const AttnProblem &p, cudaStream_t st) {
 #ifdef SPA_ATTN_TRACE
 extern "C" int spa_debug_read_trace(unsigned long long *out) {
     return (int)cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace));
+}
+extern "C" int spa_debug_read_trace2(unsigned long long *out) {
+    return (int)cudaMemcpyFromSymbol(out, g_trace2, sizeof(g_trace2));
 }
 #endif
 

@@ -59,3 +59,17 @@ print(f"TMA latency (issue -> MMA warp sees data): K {np.mean(d[:, 2] - d[:, 11]
 print("MMA side: "
       f"QK(j) issue -> P0(j) ready {np.mean(d[:, 0] - d[:, 2]):.0f} | P0 -> P1 {np.mean(d[:, 1] - d[:, 0]):.0f} | "
       f"S(j) ready - QK(j) issue {np.mean(d[:, 4] - d[:, 2]):.0f}")
+
+# per-warp view (both CTAs of cluster 0, all four lane quarters): softmax duration S(j) seen -> P halves released
+if hasattr(lib, "spa_debug_read_trace2"):
+    buf2 = (ctypes.c_ulonglong * (256 * 8 * 3))()
+    lib.spa_debug_read_trace2.argtypes = [ctypes.c_void_p]
+    assert lib.spa_debug_read_trace2(ctypes.addressof(buf2)) == 0
+    T2 = np.frombuffer(buf2, dtype=np.uint64).reshape(256, 8, 3).astype(np.int64)
+    d2 = T2[js]
+    print("per warp (CTA, quarter): mean S-seen -> 1st half / 2nd half released; leader S-seen offset vs quarter 0")
+    for slot in range(8):
+        c, q = divmod(slot, 4)
+        off = np.mean(d2[:, slot, 0] - d2[:, 0, 0]) if c == 0 else float("nan")
+        print(f"  cta {c} wq {q}: {np.mean(d2[:, slot, 1] - d2[:, slot, 0]):7.0f} {np.mean(d2[:, slot, 2] - d2[:, slot, 0]):7.0f}"
+              f"   S offset {off:7.0f}")
