@@ -460,3 +460,4 @@ __device__ __forceinline__ void tma_load_4d_2sm(const CUtensorMap *m, uint32_t b
 }  // namespace ptx
 }  // namespace spa
 
+
