@@ -8,6 +8,7 @@ timeout 900 python -m pytest tests -m gpu -q > $OUT/gpu_tests.log 2>&1; echo "rc
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1
 timeout 600 python bench.py > $OUT/bench.jsonl 2> $OUT/bench.err
 timeout 400 python bench.py --impl reference --steps 5 --warmup 3 > $OUT/bench_reference.jsonl 2> $OUT/bench_reference.err
+timeout 600 python bench.py --workload hy544p129f --steps 5 --no-cpu-baseline > $OUT/bench_hy544p.jsonl 2>> $OUT/bench.err
 timeout 300 python tools/attn_perf.py --sdpa > $OUT/attn_perf.jsonl 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"attn_fwd|copy_runs" --csv \
     --log-file $OUT/launches_bench.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
