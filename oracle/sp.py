@@ -31,13 +31,24 @@ Attn = Callable[[np.ndarray, np.ndarray, np.ndarray], np.ndarray]
 
 
 # ---------------------------------------------------------------- primitives
-def shard_seq(X: np.ndarray, P: int) -> List[np.ndarray]:
-    """X [B,S,H,D] -> P sequence shards [B,S/P,H,D] (rank r holds tokens [r*S_l,(r+1)*S_l))."""
+def shard_bounds(S: int, P: int) -> List[int]:
+    """Token bounds of P sequence shards that differ in length by at most one (R9; the SPEC's
+    ShardedTensor "differ by <= 1"): the first S % P ranks hold one token more."""
+    base, extra = divmod(S, P)
+    b = [0]
+    for r in range(P):
+        b.append(b[-1] + base + (1 if r < extra else 0))
+    return b
+
+
+def shard_seq(X: np.ndarray, P: int, uneven: bool = False) -> List[np.ndarray]:
+    """X [B,S,H,D] -> P sequence shards (rank r holds tokens [bounds[r], bounds[r+1])); equal shards of S/P
+    tokens unless uneven=True allows S % P != 0."""
     B, S, H, D = X.shape
-    if S % P:
+    if S % P and not uneven:
         raise ValueError("S % P != 0")
-    S_l = S // P
-    return [X[:, r * S_l:(r + 1) * S_l].copy() for r in range(P)]
+    b = shard_bounds(S, P)
+    return [X[:, b[r]:b[r + 1]].copy() for r in range(P)]
 
 
 def all_to_all(send: Sequence[Sequence[np.ndarray]]) -> List[List[np.ndarray]]:
@@ -61,13 +72,14 @@ def seq_to_head(shards: Sequence[np.ndarray]) -> List[np.ndarray]:
     return [np.concatenate(recv[r], axis=1) for r in range(P)]
 
 
-def head_to_seq(heads: Sequence[np.ndarray]) -> List[np.ndarray]:
+def head_to_seq(heads: Sequence[np.ndarray], bounds: Sequence[int] = None) -> List[np.ndarray]:
     """Ulysses output all-to-all (one exchange after all heads):
-    out_q[b, t, r*h+j] = R_r[b, q*S_l+t, j]."""
+    out_q[b, t, r*h+j] = R_r[b, bounds[q]+t, j] (bounds: the sequence shards, equal by default)."""
     P = len(heads)
     B, S, h, D = heads[0].shape
-    S_l = S // P
-    send = [[y[:, q * S_l:(q + 1) * S_l] for q in range(P)] for y in heads]
+    if bounds is None:
+        bounds = shard_bounds(S, P)
+    send = [[y[:, bounds[q]:bounds[q + 1]] for q in range(P)] for y in heads]
     recv = all_to_all(send)
     return [np.concatenate(recv[q], axis=2) for q in range(P)]
 
@@ -249,20 +261,22 @@ def pipesp_forward(Qs, Ks, Vs, n_stages: int, attn: Attn, return_tmod: bool = Fa
     With g=1, C=1 this is exactly the paper's per-head loop and Psi.
     """
     P = len(Qs)
-    B, S_l, H, D = Qs[0].shape
+    B, _, H, D = Qs[0].shape
     h = H // P
+    lens = [x.shape[1] for x in Qs]                 # sequence shards may differ by one token (R9)
+    starts = np.concatenate([[0], np.cumsum(lens)]).astype(int)
     G_h, C, g = stage_split(h, n_stages)
-    bounds = chunk_bounds(S_l, C)
+    cbs = [chunk_bounds(n, C) for n in lens]        # query chunk c of source p: its local [c0_p, c1_p)
     Rq, Rk, Rv = seq_to_head(Qs), seq_to_head(Ks), seq_to_head(Vs)  # leading all-to-alls
     chunks = [[[] for _ in range(C)] for _ in range(P)]  # chunks[dest][c] = list of stage pieces
     for kh in range(G_h):
         heads = list(range(kh * g, (kh + 1) * g))
-        for c, (c0, c1) in enumerate(bounds):
-            # rows of chunk c from every source block p: p*S_l + [c0, c1)
-            rows = np.concatenate([np.arange(p * S_l + c0, p * S_l + c1) for p in range(P)])
+        for c in range(C):
+            # rows of chunk c from every source block p: starts[p] + [c0_p, c1_p)
+            rows = np.concatenate([np.arange(starts[p] + cbs[p][c][0], starts[p] + cbs[p][c][1]) for p in range(P)])
             results = [_attn_heads(Rq[r], Rk[r], Rv[r], rows, heads, attn) for r in range(P)]
-            L = c1 - c0
-            send = [[results[r][:, q * L:(q + 1) * L] for q in range(P)] for r in range(P)]
+            offs = np.concatenate([[0], np.cumsum([cbs[q][c][1] - cbs[q][c][0] for q in range(P)])]).astype(int)
+            send = [[results[r][:, offs[q]:offs[q + 1]] for q in range(P)] for r in range(P)]
             recv = all_to_all(send)                      # the stage's All_to_All (Alg. 1 l.7)
             for q in range(P):
                 # pieces from src r: [B, L, g, D]; stage piece = concat over r along heads -> [B,L,P*g,D]

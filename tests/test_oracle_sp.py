@@ -187,3 +187,38 @@ def test_aco_speedup_eq3_and_pad_heads(golden_dir):
         assert abs(sp.aco_ideal_speedup(*g[key]["args"]) - g[key]["S"]) < 1e-12
     for H, n, Hp, pad in g["pad_heads"]:
         assert sp.pad_heads(H, n) == (Hp, pad)
+
+
+def test_shard_bounds_differ_by_at_most_one():
+    for S in (1, 7, 29, 118_800, 28_800):
+        for P in (1, 2, 3, 6, 7, 8):
+            if S < P:
+                continue
+            b = sp.shard_bounds(S, P)
+            lens = np.diff(b)
+            assert b[0] == 0 and b[-1] == S and lens.max() - lens.min() <= 1 and (np.diff(lens) <= 0).all()
+
+
+@pytest.mark.parametrize("P,S,stages", [(3, 29, 1), (3, 29, 2), (7, 7 * 5 + 3, 1), (4, 4 * 6 + 3, 3), (2, 9, 2)])
+def test_uneven_shards_pipesp_equals_unsharded(P, S, stages):
+    """S % P != 0 (R9: shards differ by one token; the Aco example of PAPER.md:198 runs 7 denoising GPUs):
+    Ulysses and PipeSP give unsharded attention bit for bit (same per-row routine, same data)."""
+    rng = np.random.default_rng(P * 100 + S)
+    B, H, D = 2, P * (3 if stages == 3 else 2), 4
+    Q, K, V = (rng.standard_normal((B, S, H, D)) for _ in range(3))
+    Qs, Ks, Vs = (sp.shard_seq(X, P, uneven=True) for X in (Q, K, V))
+    ref = oracle.mha_unsharded(Q, K, V)
+    assert np.array_equal(np.concatenate(sp.pipesp_forward(Qs, Ks, Vs, stages, oracle.attention_rows), axis=1), ref)
+    assert np.array_equal(np.concatenate(sp.ulysses_forward(Qs, Ks, Vs, oracle.attention_rows), axis=1), ref)
+
+
+def test_uneven_seq_to_head_labels():
+    """Label routing: rank r's head block holds every source's tokens in sequence order (P=3, S=8)."""
+    P, S, H = 3, 8, 3
+    X = (np.arange(S)[None, :, None, None] * 10 + np.arange(H)[None, None, :, None]).astype(np.float64)
+    R = sp.seq_to_head(sp.shard_seq(X, P, uneven=True))
+    for r in range(P):
+        assert np.array_equal(R[r][0, :, 0, 0], np.arange(S) * 10 + r)
+    back = sp.head_to_seq(R)
+    assert [x.shape[1] for x in back] == [3, 3, 2]
+    assert np.array_equal(np.concatenate(back, axis=1), X)
