@@ -53,7 +53,7 @@ extern "C" {
 typedef enum {
     SPA_OK = 0,
     SPA_ERR_INVALID = 1,     /* null pointer, bad enum, misaligned pointer, wrong comm kind */
-    SPA_ERR_SHAPE = 2,       /* S % n_src != 0, H % n_owners != 0, stages < 1, query chunks > S/n_src */
+    SPA_ERR_SHAPE = 2,       /* S < n_src, H % n_owners != 0, stages < 1, query chunks > shortest shard */
     SPA_ERR_UNSUPPORTED = 3, /* D not in {64, 96, 128}, op not available on this comm kind */
     SPA_ERR_CUDA = 4,        /* CUDA runtime/driver error (incl. a previous async kernel fault) */
     SPA_ERR_COMM = 5,        /* NCCL error or async communicator failure */
@@ -107,7 +107,10 @@ typedef struct {
                        collective). */
 } spa_shape;
 
-/* Validates everything synchronously.  Requirements: D in {64,96,128}; S % n_src == 0;
+/* Validates everything synchronously.  Sequence shards: source rank r holds tokens [start_r, start_r + len_r)
+ * with len_r = S/n_src + (r < S % n_src ? 1 : 0) -- equal when n_src divides S, otherwise differing by one
+ * token (R9; e.g. Aco with 7 denoising GPUs); q, k, v, out of rank r have len_r
+ * tokens.  Requirements: D in {64,96,128}; S >= n_src; (ring / USP plans: S % nranks == 0);
  * H % nranks == 0 unless pad_heads (heads are split over ALL ranks, which own contiguous head blocks);
  * 1 <= stages and C <= S/n_src (C and G_h follow from h = Hp/nranks). */
 spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *shape);

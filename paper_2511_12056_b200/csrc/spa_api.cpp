@@ -70,7 +70,6 @@ namespace {
 
 struct Split {
     int G_h, C, g;
-    std::vector<int> cb;  // chunk bounds (C+1)
     int n() const { return G_h * C; }
 };
 
@@ -88,7 +87,10 @@ struct spa_plan {
     spa_shape sh{};
     int P = 1;      // ranks owning heads (all ranks)
     int Psrc = 1;   // ranks holding sequence shards
-    int h = 1, S_l = 1;
+    int h = 1, S_l = 1;   // S_l: the longest sequence shard (buffer sizing)
+    // source rank r holds tokens [start[r], start[r] + len[r]); lengths differ by <= 1 (R9), the first S % Psrc
+    // ranks hold one token more
+    std::vector<int> len, start;
     int Hp = 1;     // heads after padding to a multiple of P (== sh.H unless shape.pad_heads)
     const int32_t *kv_len = nullptr;   // key-padding lengths, device int32 [B] (spa_plan_set_kv_len) or NULL
     // ring plans (shape.ring = 1; R21): per-rank workspace = 2 K/V receive slots + P fp32 partials + lse
@@ -127,29 +129,45 @@ Split make_split(int h, int S_l, int stages) {
     s.G_h = std::gcd(stages, h);
     s.C = stages / s.G_h;
     s.g = h / s.G_h;
-    s.cb.resize(s.C + 1);
-    for (int c = 0; c <= s.C; ++c) s.cb[c] = (int)((long long)c * S_l / s.C);
     return s;
 }
 
 bool is_source(const spa_plan *p, int r) { return r >= 0 && r < p->Psrc; }
 
 // ------------------------------------------------------------------ offsets (elements)
-// send / orecv (source side): [kh][q][b][t][jj][d], q < P, t < S_l
-long long idx_send(const spa_plan *p, const Split &s, int kh, int q, int b, int t) {
-    return ((((long long)kh * p->P + q) * p->sh.B + b) * p->S_l + t) * s.g * p->sh.D;
+// Query chunk c of source src covers its local tokens [clo(src, c), clo(src, c+1)) (R7; extents differ by <= 1).
+long long clo(const spa_plan *p, const Split &s, int src, int c) { return (long long)c * p->len[src] / s.C; }
+long long Lsrc(const spa_plan *p, const Split &s, int src, int c) { return clo(p, s, src, c + 1) - clo(p, s, src, c); }
+// rows of stage chunk c on an owner (all sources' pieces) and the rows of all chunks before c
+long long Lstage(const spa_plan *p, const Split &s, int c) {
+    long long n = 0;
+    for (int src = 0; src < p->Psrc; ++src) n += Lsrc(p, s, src, c);
+    return n;
 }
-// recvQ / O (owner side), stage (kh, c): [b][Psrc*L][jj][d] at base(kh,c)
+long long stage_prefix(const spa_plan *p, const Split &s, int c) {
+    long long n = 0;
+    for (int src = 0; src < p->Psrc; ++src) n += clo(p, s, src, c);
+    return n;
+}
+long long src_prefix(const spa_plan *p, const Split &s, int c, int src) {
+    long long n = 0;
+    for (int q = 0; q < src; ++q) n += Lsrc(p, s, q, c);
+    return n;
+}
+// send / orecv (source rank r): [kh][q][b][t][jj][d], q < P, t < len[r]
+long long idx_send(const spa_plan *p, const Split &s, int r, int kh, int q, int b, long long t) {
+    return ((((long long)kh * p->P + q) * p->sh.B + b) * p->len[r] + t) * s.g * p->sh.D;
+}
+// recvQ / O (owner side), stage (kh, c): [b][Lstage(c)][jj][d] at base(kh,c); source src's rows at src_prefix
 long long base_stage(const spa_plan *p, const Split &s, int kh, int c) {
-    return ((long long)kh * p->sh.B * p->sh.S + (long long)p->sh.B * p->Psrc * s.cb[c]) * s.g * p->sh.D;
+    return ((long long)kh * p->sh.B * p->sh.S + (long long)p->sh.B * stage_prefix(p, s, c)) * s.g * p->sh.D;
 }
 long long idx_qo(const spa_plan *p, const Split &s, int kh, int c, int b, int src) {
-    const long long L = s.cb[c + 1] - s.cb[c];
-    return base_stage(p, s, kh, c) + ((long long)b * p->Psrc * L + (long long)src * L) * s.g * p->sh.D;
+    return base_stage(p, s, kh, c) + ((long long)b * Lstage(p, s, c) + src_prefix(p, s, c, src)) * s.g * p->sh.D;
 }
 // recvK / recvV (owner side): [kh][b][S][jj][d]
 long long idx_kv(const spa_plan *p, const Split &s, int kh, int b, int src) {
-    return (((long long)kh * p->sh.B + b) * p->sh.S + (long long)src * p->S_l) * s.g * p->sh.D;
+    return (((long long)kh * p->sh.B + b) * p->sh.S + p->start[src]) * s.g * p->sh.D;
 }
 
 struct Msg {
@@ -161,42 +179,43 @@ struct Msg {
 // tensors: bitmask 1=Q 2=K 4=V.  q_recv_buf: BUF_WS (recvQ region) or BUF_XHEAD (reshard target).
 void gen_in_msgs(const spa_plan *p, const Split &s, int k, int r, int tensors, int q_recv_buf, std::vector<Msg> &m) {
     const int kh = k / s.C, c = k % s.C;
-    const long long L = s.cb[c + 1] - s.cb[c];
     const long long run = (long long)s.g * p->sh.D * 2;
     const bool kv = (c == 0);
     if (is_source(p, r)) {
+        const long long L = Lsrc(p, s, r, c), c0 = clo(p, s, r, c), n = p->len[r];
         for (int q = 0; q < p->P; ++q)
             for (int b = 0; b < p->sh.B; ++b) {
-                if (tensors & 1) m.push_back({q, 0, BUF_WS, p->off_sendQ + idx_send(p, s, kh, q, b, s.cb[c]) * 2, L * run});
-                if (kv && (tensors & 2)) m.push_back({q, 0, BUF_WS, p->off_sendK + idx_send(p, s, kh, q, b, 0) * 2, p->S_l * run});
-                if (kv && (tensors & 4)) m.push_back({q, 0, BUF_WS, p->off_sendV + idx_send(p, s, kh, q, b, 0) * 2, p->S_l * run});
+                if (tensors & 1) m.push_back({q, 0, BUF_WS, p->off_sendQ + idx_send(p, s, r, kh, q, b, c0) * 2, L * run});
+                if (kv && (tensors & 2)) m.push_back({q, 0, BUF_WS, p->off_sendK + idx_send(p, s, r, kh, q, b, 0) * 2, n * run});
+                if (kv && (tensors & 4)) m.push_back({q, 0, BUF_WS, p->off_sendV + idx_send(p, s, r, kh, q, b, 0) * 2, n * run});
             }
     }
     for (int src = 0; src < p->Psrc; ++src)
         for (int b = 0; b < p->sh.B; ++b) {
+            const long long L = Lsrc(p, s, src, c), n = p->len[src];
             if (tensors & 1) {
                 const long long rel = idx_qo(p, s, kh, c, b, src) * 2;
                 m.push_back({src, 1, q_recv_buf, (q_recv_buf == BUF_WS ? p->off_recvQ : 0) + rel, L * run});
             }
-            if (kv && (tensors & 2)) m.push_back({src, 1, BUF_WS, p->off_recvK + idx_kv(p, s, kh, b, src) * 2, p->S_l * run});
-            if (kv && (tensors & 4)) m.push_back({src, 1, BUF_WS, p->off_recvV + idx_kv(p, s, kh, b, src) * 2, p->S_l * run});
+            if (kv && (tensors & 2)) m.push_back({src, 1, BUF_WS, p->off_recvK + idx_kv(p, s, kh, b, src) * 2, n * run});
+            if (kv && (tensors & 4)) m.push_back({src, 1, BUF_WS, p->off_recvV + idx_kv(p, s, kh, b, src) * 2, n * run});
         }
 }
 
 // Output exchange of stage k as seen by rank r.  o_send_buf: BUF_WS (O region) or BUF_XHEAD.
 void gen_out_msgs(const spa_plan *p, const Split &s, int k, int r, int o_send_buf, std::vector<Msg> &m) {
     const int kh = k / s.C, c = k % s.C;
-    const long long L = s.cb[c + 1] - s.cb[c];
     const long long run = (long long)s.g * p->sh.D * 2;
     for (int src = 0; src < p->Psrc; ++src)
         for (int b = 0; b < p->sh.B; ++b) {
             const long long rel = idx_qo(p, s, kh, c, b, src) * 2;
-            m.push_back({src, 0, o_send_buf, (o_send_buf == BUF_WS ? p->off_O : 0) + rel, L * run});
+            m.push_back({src, 0, o_send_buf, (o_send_buf == BUF_WS ? p->off_O : 0) + rel, Lsrc(p, s, src, c) * run});
         }
     if (is_source(p, r)) {
+        const long long L = Lsrc(p, s, r, c), c0 = clo(p, s, r, c);
         for (int q = 0; q < p->P; ++q)
             for (int b = 0; b < p->sh.B; ++b)
-                m.push_back({q, 1, BUF_WS, p->off_orecv + idx_send(p, s, kh, q, b, s.cb[c]) * 2, L * run});
+                m.push_back({q, 1, BUF_WS, p->off_orecv + idx_send(p, s, r, kh, q, b, c0) * 2, L * run});
     }
 }
 
@@ -208,9 +227,9 @@ int real_heads(const spa_plan *p, const Split &s, int q, int kh) {
 // Pack (source rank): send[kh][q][b][t][jj][d] = X[b][t][q*h + kh*g + jj][d].
 // One 4-level job when every head group is complete; with padded heads one job per (kh, q) that copies only
 // the real heads of the group (pad-head slots of the send buffer are never written nor read as results).
-void pack_jobs(const spa_plan *p, const Split &s, const void *x, long long dst_off, uint8_t *ws,
+void pack_jobs(const spa_plan *p, const Split &s, int r, const void *x, long long dst_off, uint8_t *ws,
                std::vector<CopyJob> &out) {
-    const long long D2 = (long long)p->sh.D * 2, H = p->sh.H;
+    const long long D2 = (long long)p->sh.D * 2, H = p->sh.H, n = p->len[r];   // source rank r: n tokens
     const long long run = s.g * D2;
     // x == NULL / ws == NULL (describe): the job pointers hold plain byte offsets
     const uintptr_t xb = reinterpret_cast<uintptr_t>(x);
@@ -220,11 +239,11 @@ void pack_jobs(const spa_plan *p, const Split &s, const void *x, long long dst_o
         CopyJob j{};
         j.src = at(xb, 0);
         j.dst = at(wb, 0);
-        j.count[0] = s.G_h; j.count[1] = p->P; j.count[2] = p->sh.B; j.count[3] = p->S_l;
-        j.src_stride[0] = s.g * D2; j.src_stride[1] = p->h * D2; j.src_stride[2] = p->S_l * H * D2;
+        j.count[0] = s.G_h; j.count[1] = p->P; j.count[2] = p->sh.B; j.count[3] = n;
+        j.src_stride[0] = s.g * D2; j.src_stride[1] = p->h * D2; j.src_stride[2] = n * H * D2;
         j.src_stride[3] = H * D2;
-        j.dst_stride[3] = run; j.dst_stride[2] = p->S_l * run; j.dst_stride[1] = p->sh.B * p->S_l * run;
-        j.dst_stride[0] = p->P * p->sh.B * p->S_l * run;
+        j.dst_stride[3] = run; j.dst_stride[2] = n * run; j.dst_stride[1] = p->sh.B * n * run;
+        j.dst_stride[0] = p->P * p->sh.B * n * run;
         j.run_bytes = run;
         out.push_back(j);
         return;
@@ -235,19 +254,19 @@ void pack_jobs(const spa_plan *p, const Split &s, const void *x, long long dst_o
             if (nreal == 0) continue;
             CopyJob j{};
             j.src = at(xb, (q * p->h + kh * s.g) * D2);
-            j.dst = at(wb, idx_send(p, s, kh, q, 0, 0) * 2);
-            j.count[0] = 1; j.count[1] = 1; j.count[2] = p->sh.B; j.count[3] = p->S_l;
-            j.src_stride[2] = p->S_l * H * D2; j.src_stride[3] = H * D2;
-            j.dst_stride[2] = p->S_l * run; j.dst_stride[3] = run;
+            j.dst = at(wb, idx_send(p, s, r, kh, q, 0, 0) * 2);
+            j.count[0] = 1; j.count[1] = 1; j.count[2] = p->sh.B; j.count[3] = n;
+            j.src_stride[2] = n * H * D2; j.src_stride[3] = H * D2;
+            j.dst_stride[2] = n * run; j.dst_stride[3] = run;
             j.run_bytes = nreal * D2;
             out.push_back(j);
         }
 }
 // Unpack (source rank), Psi_g fused: out[b][t][q*h + kh*g + jj][d] = orecv[kh][q][b][t][jj][d]  (a5)
-void unpack_jobs(const spa_plan *p, const Split &s, uint8_t *ws, long long src_off, void *outp,
+void unpack_jobs(const spa_plan *p, const Split &s, int r, uint8_t *ws, long long src_off, void *outp,
                  std::vector<CopyJob> &out) {
     const size_t first = out.size();
-    pack_jobs(p, s, nullptr, 0, nullptr, out);
+    pack_jobs(p, s, r, nullptr, 0, nullptr, out);
     for (size_t i = first; i < out.size(); ++i) {
         CopyJob &j = out[i];
         std::swap(j.src_stride, j.dst_stride);
@@ -382,7 +401,7 @@ spa_status run_attention(Exec &x, int k, cudaStream_t st) {
     spa_plan *p = x.p;
     const Split &s = *x.s;
     const int kh = k / s.C, c = k % s.C;
-    const long long L = s.cb[c + 1] - s.cb[c];
+    const long long Lst = Lstage(p, s, c);   // the stage's query rows (every source's chunk c)
     const int nr = (p->comm->kind == KIND_LOOPBACK) ? p->P : 1;
     for (int rr = 0; rr < nr; ++rr) {
         const int r = (p->comm->kind == KIND_LOOPBACK) ? rr : p->comm->rank;
@@ -394,10 +413,10 @@ spa_status run_attention(Exec &x, int k, cudaStream_t st) {
         a.k = ws + p->off_recvK + idx_kv(p, s, kh, 0, 0) * 2;
         a.v = ws + p->off_recvV + idx_kv(p, s, kh, 0, 0) * 2;
         a.o = ws + p->off_O + base_stage(p, s, kh, c) * 2;
-        a.B = p->sh.B; a.Sq = (int)(p->Psrc * L); a.Skv = p->sh.S; a.n_heads = nreal; a.D = p->sh.D;
+        a.B = p->sh.B; a.Sq = (int)Lst; a.Skv = p->sh.S; a.n_heads = nreal; a.D = p->sh.D;
         a.kv_len = p->kv_len;
         a.q_tok_stride = a.kv_tok_stride = a.o_tok_stride = (long long)s.g * p->sh.D;
-        a.q_batch_stride = a.o_batch_stride = p->Psrc * L * s.g * p->sh.D;
+        a.q_batch_stride = a.o_batch_stride = Lst * s.g * p->sh.D;
         a.kv_batch_stride = (long long)p->sh.S * s.g * p->sh.D;
         SPA_CHECK_CUDA(launch_attention(a, st));
         ++p->attn_launches;
@@ -412,9 +431,9 @@ spa_status run_pack(Exec &x) {
     for (int i = 0; i < nr; ++i) {
         const int r = (p->comm->kind == KIND_LOOPBACK) ? i : p->comm->rank;
         uint8_t *ws = resolve(x, r, BUF_WS, 0);
-        if (x.in_tensors & 1) pack_jobs(p, *x.s, x.ptr.q[i], p->off_sendQ, ws, jobs);
-        if (x.in_tensors & 2) pack_jobs(p, *x.s, x.ptr.k[i], p->off_sendK, ws, jobs);
-        if (x.in_tensors & 4) pack_jobs(p, *x.s, x.ptr.v[i], p->off_sendV, ws, jobs);
+        if (x.in_tensors & 1) pack_jobs(p, *x.s, r, x.ptr.q[i], p->off_sendQ, ws, jobs);
+        if (x.in_tensors & 2) pack_jobs(p, *x.s, r, x.ptr.k[i], p->off_sendK, ws, jobs);
+        if (x.in_tensors & 4) pack_jobs(p, *x.s, r, x.ptr.v[i], p->off_sendV, ws, jobs);
     }
     if (jobs.empty()) return SPA_OK;
     SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sc, &p->copy_launches));
@@ -427,7 +446,7 @@ spa_status run_unpack(Exec &x) {
     const int nr = (p->comm->kind == KIND_LOOPBACK) ? p->Psrc : (is_source(p, p->comm->rank) ? 1 : 0);
     for (int i = 0; i < nr; ++i) {
         const int r = (p->comm->kind == KIND_LOOPBACK) ? i : p->comm->rank;
-        unpack_jobs(p, *x.s, resolve(x, r, BUF_WS, 0), p->off_orecv, x.ptr.out[i], jobs);
+        unpack_jobs(p, *x.s, r, resolve(x, r, BUF_WS, 0), p->off_orecv, x.ptr.out[i], jobs);
     }
     if (jobs.empty()) return SPA_OK;
     SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sc, &p->copy_launches));
@@ -813,7 +832,7 @@ spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *sha
     const int P = comm->nranks;
     const int Psrc = s.n_src == 0 ? P : s.n_src;
     if (Psrc < 1 || Psrc > P) return fail(SPA_ERR_SHAPE, "n_src must be in [0, nranks]");
-    if (s.S % Psrc) return fail(SPA_ERR_SHAPE, "S must be divisible by the number of source ranks");
+    if (s.S < Psrc) return fail(SPA_ERR_SHAPE, "fewer tokens than source ranks");
     if (s.pad_heads != 0 && s.pad_heads != 1) return fail(SPA_ERR_INVALID, "pad_heads must be 0 or 1");
     if (s.ring != 0 && s.ring != 1) return fail(SPA_ERR_INVALID, "ring must be 0 or 1");
     if (s.ulysses < 0 || (!s.ring && s.ulysses > 1)) return fail(SPA_ERR_INVALID, "ulysses degree needs ring = 1");
@@ -843,9 +862,18 @@ spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *sha
     spa_plan *p = new spa_plan;
     p->comm = comm; p->sh = s; p->P = P; p->Psrc = Psrc;
     p->Hp = (s.H + P - 1) / P * P;
-    p->h = p->Hp / P; p->S_l = s.S / Psrc;
+    p->h = p->Hp / P;
+    // sequence shards differ by at most one token: the first S % Psrc source ranks hold one more (R9)
+    p->len.resize(Psrc);
+    p->start.resize(Psrc + 1);
+    p->start[0] = 0;
+    for (int r = 0; r < Psrc; ++r) {
+        p->len[r] = s.S / Psrc + (r < s.S % Psrc ? 1 : 0);
+        p->start[r + 1] = p->start[r] + p->len[r];
+    }
+    p->S_l = p->len[0];   // the longest shard (buffer sizing)
     p->split = make_split(p->h, p->S_l, s.stages);
-    if (p->split.C > p->S_l) {
+    if (p->split.C > p->len[Psrc - 1]) {
         delete p;
         return fail(SPA_ERR_SHAPE, "more query chunks than local tokens");
     }
@@ -1251,7 +1279,7 @@ spa_status spa_plan_describe_pack(const spa_plan *plan, int rank, spa_copy_desc 
     const long long offs[3] = {plan->off_sendQ, plan->off_sendK, plan->off_sendV};
     for (int t = 0; t < 3; ++t) {
         std::vector<CopyJob> jobs;
-        pack_jobs(plan, plan->split, nullptr, 0, nullptr, jobs);
+        pack_jobs(plan, plan->split, rank, nullptr, 0, nullptr, jobs);
         for (const CopyJob &j : jobs) {
             if (*n >= max) return fail(SPA_ERR_INVALID, "describe: output too small");
             // job pointers are offsets from NULL here: source offset into the user buffer, destination into ws
@@ -1268,7 +1296,7 @@ spa_status spa_plan_describe_unpack(const spa_plan *plan, int rank, spa_copy_des
     *n = 0;
     if (plan->P == 1 || !is_source(plan, rank)) return SPA_OK;
     std::vector<CopyJob> jobs;
-    unpack_jobs(plan, plan->split, nullptr, 0, nullptr, jobs);
+    unpack_jobs(plan, plan->split, rank, nullptr, 0, nullptr, jobs);
     for (const CopyJob &j : jobs) {
         if (*n >= max) return fail(SPA_ERR_INVALID, "describe: output too small");
         out[(*n)++] = to_desc(j, BUF_WS, rank, plan->off_orecv + (long long)reinterpret_cast<uintptr_t>(j.src),
@@ -1300,14 +1328,14 @@ spa_status spa_plan_describe_attention(const spa_plan *p, int stage, int rank, s
     if (stage < 0 || stage >= p->split.n() || rank < 0 || rank >= p->P) return fail(SPA_ERR_INVALID, "bad stage/rank");
     const Split &s = p->split;
     const int kh = stage / s.C, c = stage % s.C;
-    const long long L = s.cb[c + 1] - s.cb[c];
+    const long long Lst = Lstage(p, s, c);
     out->q_off = p->off_recvQ + base_stage(p, s, kh, c) * 2;
     out->k_off = p->off_recvK + idx_kv(p, s, kh, 0, 0) * 2;
     out->v_off = p->off_recvV + idx_kv(p, s, kh, 0, 0) * 2;
     out->o_off = p->off_O + base_stage(p, s, kh, c) * 2;
-    out->B = p->sh.B; out->Sq = (int)(p->Psrc * L); out->Skv = p->sh.S; out->n_heads = real_heads(p, s, rank, kh);
+    out->B = p->sh.B; out->Sq = (int)Lst; out->Skv = p->sh.S; out->n_heads = real_heads(p, s, rank, kh);
     out->q_tok_stride = out->kv_tok_stride = (long long)s.g * p->sh.D;
-    out->q_batch_stride = p->Psrc * L * s.g * p->sh.D;
+    out->q_batch_stride = Lst * s.g * p->sh.D;
     out->kv_batch_stride = (long long)p->sh.S * s.g * p->sh.D;
     return SPA_OK;
 }

@@ -30,7 +30,7 @@ def test_status_strings_and_pad_heads():
 
 @pytest.mark.parametrize("shape,err", [
     (dict(B=1, S=256, H=4, D=80), 3),            # D unsupported
-    (dict(B=1, S=255, H=4, D=64), 2),            # S % P
+    (dict(B=1, S=1, H=4, D=64), 2),              # fewer tokens than ranks
     (dict(B=1, S=256, H=3, D=64), 2),            # H % P
     (dict(B=1, S=256, H=4, D=64, stages=0), 2),  # stages < 1
     (dict(B=1, S=4, H=2, D=64, stages=8), 2),    # more query chunks than local tokens
@@ -124,14 +124,17 @@ def test_stage_split_and_workspace():
 
 
 def _labels(B, S, H, D, P, n_src=None):
+    """per-source label shards (uneven when n_src does not divide S: the first S % n_src ranks get one more)"""
     n_src = n_src or P
-    S_l = S // n_src
+    bnd = [0]
+    for r in range(n_src):
+        bnd.append(bnd[-1] + S // n_src + (1 if r < S % n_src else 0))
     b = np.arange(B)[:, None, None, None]
     s = np.arange(S)[None, :, None, None]
     k = np.arange(H)[None, None, :, None]
     d = np.arange(D)[None, None, None, :]
     X = ((b * 7 + s * 131 + k * 17 + d) % 65521).astype(np.uint16)
-    return [np.ascontiguousarray(X[:, r * S_l:(r + 1) * S_l]).view(np.uint8).reshape(-1) for r in range(n_src)], X
+    return [np.ascontiguousarray(X[:, bnd[r]:bnd[r + 1]]).view(np.uint8).reshape(-1) for r in range(n_src)], X
 
 
 @pytest.mark.parametrize("P,H,S,B,stages", [
@@ -145,6 +148,32 @@ def test_host_path_routes_every_element_home(P, H, S, B, stages):
     outs = hostsim.run_path(plans, xs, xs, xs)
     for r in range(P):
         assert np.array_equal(outs[r], xs[r]), r
+
+
+@pytest.mark.parametrize("P,H,S,B,stages", [
+    (3, 6, 29, 1, 1), (3, 6, 29, 2, 2), (7, 7, 7 * 5 + 3, 1, 1), (4, 8, 4 * 6 + 3, 1, 4), (8, 24, 8 * 11 + 7, 1, 24),
+    (2, 4, 9, 1, 2),
+])
+def test_host_path_uneven_shards(P, H, S, B, stages):
+    """S % P != 0 (R9): shards differ by one token; every element still routes home."""
+    D = 64
+    plans = [spa.Plan(spa.Comm.host(P, r), B, S, H, D, stages=stages) for r in range(P)]
+    xs, _ = _labels(B, S, H, D, P)
+    outs = hostsim.run_path(plans, xs, xs, xs)
+    for r in range(P):
+        assert np.array_equal(outs[r], xs[r]), r
+
+
+@pytest.mark.parametrize("n_src,N,H,S,stages", [(7, 8, 24, 7 * 12 + 3, 1), (7, 8, 24, 7 * 12 + 5, 3)])
+def test_host_path_aco_seven_plus_one(n_src, N, H, S, stages):
+    """The paper's Aco example: 24 heads, 7 denoising GPUs + 1 decoding GPU -- owners hold 3
+    heads each, the sequence is sharded over 7 (unevenly)."""
+    B, D = 1, 64
+    plans = [spa.Plan(spa.Comm.host(N, r), B, S, H, D, stages=stages, n_src=n_src) for r in range(N)]
+    xs, _ = _labels(B, S, H, D, N, n_src)
+    outs = hostsim.run_path(plans, xs, xs, xs)
+    for r in range(n_src):
+        assert np.array_equal(outs[r], xs[r])
 
 
 @pytest.mark.parametrize("n_src,N,H,stages", [(6, 8, 24, 1), (6, 8, 24, 3), (3, 4, 8, 2), (1, 2, 2, 1)])

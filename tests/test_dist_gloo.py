@@ -65,12 +65,14 @@ def _worker(rank, world, port, cases, result):
     for (B, S, H, D, stages, n_src, pad) in cases:
         plan = spa.Plan(spa.Comm.host(world, rank), B, S, H, D, stages=stages, n_src=n_src, pad_heads=pad)
         nsrc = n_src or world
-        S_l = S // nsrc
+        bnd = [0]
+        for r in range(nsrc):   # uneven shards when nsrc does not divide S (first S % nsrc ranks longer)
+            bnd.append(bnd[-1] + S // nsrc + (1 if r < S % nsrc else 0))
         X = ((np.arange(B * S * H * D) * 2654435761) % 65521).astype(np.uint16).reshape(B, S, H, D)
         ws = np.zeros(plan.workspace_bytes, dtype=np.uint8)
         x = None
         if rank < nsrc:
-            x = np.ascontiguousarray(X[:, rank * S_l:(rank + 1) * S_l]).view(np.uint8).reshape(-1)
+            x = np.ascontiguousarray(X[:, bnd[rank]:bnd[rank + 1]]).view(np.uint8).reshape(-1)
             for d in plan.describe_pack(rank):
                 hostsim.run_copy(d, x, ws)
         G_h, C, g = plan.stage_split
@@ -93,7 +95,7 @@ def test_two_process_gloo_exchange():
     # (B, S, H, D, stages, n_src, pad_heads); the last two: H odd over 2 ranks with head padding
     cases = [(1, 64, 4, 64, 1, 0, 0), (1, 64, 4, 64, 2, 0, 0), (2, 64, 4, 96, 4, 0, 0), (1, 128, 8, 128, 8, 0, 0),
              (1, 96, 6, 64, 6, 0, 0), (1, 48, 2, 64, 1, 1, 0), (2, 48, 4, 64, 2, 1, 0), (1, 64, 3, 64, 2, 0, 1),
-             (2, 64, 5, 96, 3, 0, 1)]
+             (2, 64, 5, 96, 3, 0, 1), (1, 63, 4, 64, 2, 0, 0), (2, 63, 6, 64, 3, 1, 0)]
     world = 2
     ctx = mp.get_context("spawn")
     result = ctx.Array("i", [0] * world)

@@ -152,3 +152,27 @@ def test_key_padding_mask_fullsize():
     torch.cuda.synchronize()
     del ws
     assert torch.equal(torch.cat(outs, dim=1).view(torch.int16), single.view(torch.int16))
+
+
+def test_aco_720p_seven_plus_one():
+    """The paper's Aco example at configs[3] size: S = 118,800 over 7 denoising ranks (uneven:
+    16,972 / 16,971 tokens), 24 heads over 7 + 1 owners; bit-identical to the single-GPU kernel."""
+    w = synthgen.WORKLOADS["hy720p129f"]
+    q, k, v = _gen(w.B, w.S, w.H, w.D, seed=4)
+    single = spa.attention(q, k, v)
+    plan = spa.Plan(spa.Comm.loopback(8), w.B, w.S, w.H, w.D, stages=3, n_src=7)
+    shards, t = [[], [], []], 0
+    for r in range(7):
+        ln = w.S // 7 + (1 if r < w.S % 7 else 0)
+        for i, x in enumerate((q, k, v)):
+            shards[i].append(x[:, t:t + ln].contiguous())
+        t += ln
+    outs = [torch.empty_like(x) for x in shards[0]]
+    ws = plan.workspace()
+    spa.spa_aco_attention_local(plan, *shards, outs, ws)
+    torch.cuda.synchronize()
+    del ws
+    out = torch.cat(outs, dim=1)
+    assert torch.equal(out.view(torch.int16), single.view(torch.int16))
+    ma, rl = _check_rows(q, k, v, out, _sample(w.S, 7, n=16, seed=6), heads=[21])
+    assert ma <= U.MAX_ABS and rl <= U.REL_L2, (ma, rl)

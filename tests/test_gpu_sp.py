@@ -13,8 +13,14 @@ pytestmark = [pytest.mark.gpu, pytest.mark.timeout(900)]
 
 
 def _shards(x, n):
-    S_l = x.shape[1] // n
-    return [x[:, r * S_l:(r + 1) * S_l].contiguous() for r in range(n)]
+    """sequence shards; uneven (first S % n ranks one token longer) when n does not divide S"""
+    S = x.shape[1]
+    out, t = [], 0
+    for r in range(n):
+        ln = S // n + (1 if r < S % n else 0)
+        out.append(x[:, t:t + ln].contiguous())
+        t += ln
+    return out
 
 
 def _u16(t):
@@ -133,3 +139,30 @@ def test_aco_busy_returns_busy():
     with pytest.raises(spa.SpaError) as e:
         spa.spa_aco_attention_local(plan, [x] * 6, [x] * 6, [x] * 6, [x] * 6, plan.workspace())
     assert e.value.status == 6
+
+
+@pytest.mark.parametrize("P,S,stages", [(3, 3 * 100 + 2, 1), (3, 3 * 100 + 2, 3), (7, 7 * 64 + 5, 1), (8, 8 * 93 + 7, 6)])
+def test_uneven_shards_bit_identical(P, S, stages):
+    """S % P != 0 (R9): shards differ by one token; PipeSP and Ulysses still give the single-GPU bits."""
+    B, D = 2, 96
+    H = 3 * P
+    q, k, v = U.qkv(B, S, H, D, seed=S)
+    single = spa.attention(q, k, v)
+    out = _pipesp(P, q, k, v, stages)
+    assert torch.equal(out.view(torch.int16), single.view(torch.int16))
+    uly = _pipesp(P, q, k, v, 1, ulysses=True)
+    assert torch.equal(uly.view(torch.int16), single.view(torch.int16))
+    U.assert_close(out, U.oracle_mha(q, k, v))
+
+
+@pytest.mark.parametrize("stages", [1, 3])
+def test_aco_seven_plus_one(stages):
+    """The paper's Aco example: H = 24 with 7 denoising GPUs, which Ulysses could only run with
+    padding to 28 heads; with a decoding GPU as co-processor the 24 heads split 3 per owner over 8 GPUs and
+    the sequence over 7 (unevenly)."""
+    B, S, H, D = 1, 7 * 90 + 4, 24, 128
+    q, k, v = U.qkv(B, S, H, D, seed=77)
+    single = spa.attention(q, k, v)
+    out = _pipesp(8, q, k, v, stages, n_src=7)
+    assert torch.equal(out.view(torch.int16), single.view(torch.int16))
+    U.assert_close(out, U.oracle_mha(q, k, v))
