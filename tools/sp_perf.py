@@ -28,12 +28,15 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--aco", type=int, default=0, help="n_src for an Aco plan (0 = PipeSP)")
     ap.add_argument("--ring", action="store_true", help="Ring-Attention plan instead of PipeSP")
+    ap.add_argument("--pad", action="store_true", help="head padding when H % P != 0 (PAPER.md:196-199)")
     args = ap.parse_args()
     w = synthgen.WORKLOADS[args.workload]
     B, S, H, D, P = w.B, w.S, w.H, w.D, args.P
     nsrc = args.aco or P
-    S_l = S // nsrc
-    shards = [[synthgen.gen_qkv_shard(0, t, (B, S, H, D), r * S_l, (r + 1) * S_l, device="cuda") for r in range(nsrc)]
+    bnd = [0]
+    for r in range(nsrc):   # uneven shards when nsrc does not divide S (first S % nsrc ranks one token longer)
+        bnd.append(bnd[-1] + S // nsrc + (1 if r < S % nsrc else 0))
+    shards = [[synthgen.gen_qkv_shard(0, t, (B, S, H, D), bnd[r], bnd[r + 1], device="cuda") for r in range(nsrc)]
               for t in range(3)]
     outs = [torch.empty_like(x) for x in shards[0]]
     flops = 4.0 * B * S * S * H * D
@@ -69,7 +72,7 @@ def main():
         plan.close()
         return
     for st in [int(x) for x in args.stages.split(",")]:
-        plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=st, n_src=args.aco)
+        plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=st, n_src=args.aco, pad_heads=args.pad)
         ws = plan.workspace()
         call = spa.spa_aco_attention_local if args.aco else spa.spa_pipesp_attention_local
         for _ in range(2):
