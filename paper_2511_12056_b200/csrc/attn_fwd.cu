@@ -11,7 +11,7 @@
 // (D/2 columns), so each SM takes in half of the K/V stream; only the leader CTA issues MMAs.
 //   * TMEM: three S buffers (fp32, 128 columns each) at [0,128), [128,256), [256,384) and ONE O
 //     accumulator at [384, 384+D).  KV tile j goes to S buffer j%3 and is handled by softmax group j%3
-//     (groups = warps 4g..4g+3, one warp per TMEM lane quarter = SM sub-partition).  Three S buffers make
+//     (group g = warps 4+4g..7+4g, one warp per TMEM lane quarter = SM sub-partition).  Three S buffers make
 //     three independent S -> softmax -> PV chains, so the tensor pipe always has a QK^T or PV product
 //     queued while a group is in its softmax (each group has three tiles of MMA time for one tile of
 //     softmax; the v3 design with two chains was latency-bound: softmax warps idled a third of the time
@@ -22,11 +22,11 @@
 //     it by more than 2^8 (conditional rescale); then the group that moved it waits for PV(j-1) and rescales
 //     O in TMEM before releasing P(j).  Each group keeps its own partial row sum l_g relative to the last
 //     max it saw; the epilogue merges them.
-//   warp 12 TMA producer (warps 13, 14 idle): Q once, then K/V tiles through an NS-slot smem ring in consumption order
+//   warp 0 TMA producer (warps 1, 2 idle): Q once, then K/V tiles through an NS-slot smem ring in consumption order
 //           (K0, K1, K2, V0, K3, V1, K4, ...); each CTA of the pair loads only its half of every tile (64 keys
 //           of K, D/2 columns of V), counted on the leader's full barrier.
-//   warp 15 TMEM allocator (cta_group::2, both CTAs) + tcgen05.mma issuer (leader CTA, one elected lane; highest
-//           warp id = scheduler priority): S(j) = Q K_j^T (SS, M=256, N=128) into S buffer j%3 of both CTAs;
+//   warp 3 TMEM allocator (cta_group::2, both CTAs) + tcgen05.mma issuer (leader CTA, one elected lane; the
+//           softmax warps 4.. have the higher ids = scheduler priority): S(j) = Q K_j^T (SS, M=256, N=128) into S buffer j%3 of both CTAs;
 //           O += P(j) V_j (TS: P from each CTA's TMEM, V MN-major, N = D in one instruction), released in two
 //           key halves once the softmax warps of BOTH CTAs arrived (8 arrivals on the leader's barrier);
 //           S(j+3) is issued right after PV(j).  Commits are multicast to both CTAs' barriers.
@@ -101,12 +101,14 @@ struct Cfg {
 #endif
     static constexpr int HALF = BN / 2;                  // keys per P release (64 or 48)
     static constexpr int NUM_SOFTMAX_WARPS = 4 * NG;
-    // NG warpgroups of softmax warps, then {producer, 2 idle, MMA}.  The last warpgroup gives its registers to
-    // the softmax warps (setmaxnreg): per SM sub-partition NG x SOFTMAX_REGS + AUX_REGS <= (NG + 1) x LAUNCH_REGS.
-    static constexpr int PRODUCER_WARP = NUM_SOFTMAX_WARPS;
-    // The MMA issuer has the highest warp id: the warp scheduler favours higher ids, and its few instructions
-    // must not queue behind the softmax warps that share its SM sub-partition.
-    static constexpr int MMA_WARP = NUM_SOFTMAX_WARPS + 3;
+    // Warpgroup 0 = {producer, 2 idle, MMA issuer}, then NG warpgroups of softmax warps.  Warpgroup 0 gives its
+    // registers to the softmax warps (setmaxnreg): per SM sub-partition NG x SOFTMAX_REGS + AUX_REGS <=
+    // (NG + 1) x LAUNCH_REGS.  The softmax warps have the higher warp ids, i.e. the scheduler's priority over the
+    // producer and MMA warps that share SM sub-partitions 0 and 3 with them (measured +0.2..1.4 % over the
+    // opposite order; the per-warp trace shows those two lane quarters are the slowest).
+    static constexpr int AUX_BASE = 0, SM_BASE = 4;
+    static constexpr int PRODUCER_WARP = AUX_BASE;
+    static constexpr int MMA_WARP = AUX_BASE + 3;
     static constexpr int NUM_THREADS = (NUM_SOFTMAX_WARPS + 4) * 32;
     // setmaxnreg only moves registers within the CTA's launch allocation (65536 / NUM_THREADS rounded down to
     // a multiple of 8 per thread: 128 for 512 threads, 96 for 640), so the split must fit that pool.
@@ -384,10 +386,10 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1)
                 if (j + NG < n_kv) issue_qk(j + NG);
             }
         }
-    } else if (warp < NUM_SOFTMAX_WARPS) {
+    } else if (warp >= C::SM_BASE && warp < C::SM_BASE + NUM_SOFTMAX_WARPS) {
         // ------------------------------------------------------------ softmax / correction / epilogue
         ptx::setmaxnreg_inc<C::SOFTMAX_REGS>();
-        const int g = warp >> 2;                       // softmax group: KV tiles j with j % NG == g
+        const int g = (warp - C::SM_BASE) >> 2;        // softmax group: KV tiles j with j % NG == g
         const int wq = warp & 3;                       // TMEM lane quarter this warp may access (= SMSP)
         const int row = wq * 32 + lane;                // row within the tile
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
