@@ -166,3 +166,31 @@ def test_aco_seven_plus_one(stages):
     out = _pipesp(8, q, k, v, stages, n_src=7)
     assert torch.equal(out.view(torch.int16), single.view(torch.int16))
     U.assert_close(out, U.oracle_mha(q, k, v))
+
+
+def test_two_plans_on_two_streams_concurrently():
+    """Stream semantics (include/spa.h): each call is ordered on the caller's stream; two plans driven from two
+    streams at once (their comm streams, events and workspaces are separate) both give the single-GPU bits."""
+    B, S, H, D = 1, 4 * 200, 8, 128
+    q, k, v = U.qkv(B, S, H, D, seed=123)
+    single = spa.attention(q, k, v)
+    q2, k2, v2 = U.qkv(B, S, H, D, seed=321)
+    single2 = spa.attention(q2, k2, v2)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    pa = spa.Plan(spa.Comm.loopback(4), B, S, H, D, stages=2)
+    pb = spa.Plan(spa.Comm.loopback(4), B, S, H, D, stages=4)
+    wa, wb = pa.workspace(), pb.workspace()
+    outs_a = [torch.empty_like(t) for t in _shards(q, 4)]
+    outs_b = [torch.empty_like(t) for t in _shards(q2, 4)]
+    with torch.cuda.stream(s1):
+        ia = [_shards(x, 4) for x in (q, k, v)]
+    with torch.cuda.stream(s2):
+        ib = [_shards(x, 4) for x in (q2, k2, v2)]
+    torch.cuda.synchronize()
+    for _ in range(3):
+        spa.spa_pipesp_attention_local(pa, *ia, outs_a, wa, s1)
+        spa.spa_pipesp_attention_local(pb, *ib, outs_b, wb, s2)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(outs_a, 1).view(torch.int16), single.view(torch.int16))
+    assert torch.equal(torch.cat(outs_b, 1).view(torch.int16), single2.view(torch.int16))
