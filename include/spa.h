@@ -128,7 +128,11 @@ spa_status spa_plan_destroy(spa_plan *plan);
  *   SPA_OPT_COPROC_BUSY 1 -> the decoding group is busy (Fig. 4 prompt-2 stage): spa_aco_*
  *                          return SPA_ERR_BUSY without enqueueing; the caller runs PipeSP on
  *                          the denoising sub-group instead */
-enum { SPA_OPT_PROFILE = 1, SPA_OPT_SKIP_COMM = 2, SPA_OPT_COPROC_BUSY = 3 };
+/*   SPA_OPT_DIRECT    1 -> direct transport: the pack stores straight into the
+ *                          owners' receive regions and the attention epilogue stores each output row straight
+ *                          into its source rank's output (no staging, exchange copies or unpack).  Loopback
+ *                          plans only for now (the NVLink version needs registered NCCL windows); same bits. */
+enum { SPA_OPT_PROFILE = 1, SPA_OPT_SKIP_COMM = 2, SPA_OPT_COPROC_BUSY = 3, SPA_OPT_DIRECT = 4 };
 spa_status spa_plan_set_option(spa_plan *plan, int option, int value);
 
 /* Key-padding mask for the following SP calls of this plan (Alg. 1's attention_mask, PAPER.md:85 and :90,

@@ -554,6 +554,12 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1)
         const bool valid = srow < args.Sq;      // tcgen05.ld is warp-collective: every lane loads, valid lanes store
         const long long oidx = (long long)b * args.o_batch_stride + srow * args.o_tok_stride + (long long)head * D;
         uint4 *dst = reinterpret_cast<uint4 *>(args.O + oidx);
+        if (args.n_dst > 0) {   // direct transport: this row belongs to source rank i's output buffer
+            int i = 0;
+            while (i + 1 < args.n_dst && srow >= args.row_begin[i + 1]) ++i;
+            dst = reinterpret_cast<uint4 *>(args.dst[i] + (long long)b * args.dst_batch_stride[i] +
+                                            (srow - args.row_begin[i]) * args.o_tok_stride + (long long)head * D);
+        }
         // ring / merge support: the row's log-sum-exp of the scaled scores, ln sum_t exp(q.k_t / sqrt(D)) =
         // (running max + log2 l) * ln 2 in the kernel's base-2 domain; -inf for a row without valid keys
         if (args.lse && valid && g == 0)
@@ -677,6 +683,13 @@ cudaError_t launch_d(const AttnProblem &p, cudaStream_t st) {
     a.O32 = reinterpret_cast<float *>(p.o32);
     a.lse = p.lse;
     a.lse_heads = p.n_heads;
+    a.n_dst = p.n_dst;
+    for (int i = 0; i < kMaxDst; ++i) {
+        a.dst[i] = reinterpret_cast<__nv_bfloat16 *>(p.dst[i]);
+        a.dst_batch_stride[i] = p.dst_batch_stride[i];
+        a.row_begin[i] = p.row_begin[i];
+    }
+    a.row_begin[kMaxDst] = p.row_begin[kMaxDst];
     // CTA pairs (adjacent query tiles of one head) run each MMA as one cta_group::2 instruction; an odd tile
     // count gets one extra all-out-of-range tile (zero-filled Q, rows never stored) to complete the last pair.
     const int qtiles = (p.Sq + BM - 1) / BM;

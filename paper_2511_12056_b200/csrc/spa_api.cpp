@@ -110,7 +110,7 @@ struct spa_plan {
     long long off_recvQ = 0, off_recvK = 0, off_recvV = 0, off_O = 0;
     long long ws_rank_bytes = 0;
     // options
-    bool profile = false, skip_comm = false, coproc_busy = false;
+    bool profile = false, skip_comm = false, coproc_busy = false, direct = false;
     // runtime resources (lazy)
     std::vector<cudaEvent_t> sync_ev;  // scheduling events (no timing)
     std::vector<cudaEvent_t> prof_ev;  // timing events
@@ -470,6 +470,106 @@ void finish_profile(spa_plan *p, const Prof &pr) {
     p->have_profile = true;
 }
 
+// Direct transport (loopback model): every source's pack stores its runs straight into
+// the owners' receive regions (no send staging, no exchange), and every stage's attention epilogue stores each
+// output row straight into its source rank's [B, S_l, H, D] output at head k_orig (Psi_g and the output
+// exchange fused: no orecv, no unpack).  On NVLink the same jobs / row tables use peer pointers of registered
+// NCCL windows plus a per-stage barrier; on one GPU the "peers" are the virtual ranks' local buffers.
+spa_status execute_direct(Exec &x) {
+    spa_plan *p = x.p;
+    const Split &s = *x.s;
+    const int N = s.n();
+    const long long D2 = (long long)p->sh.D * 2, H = p->sh.H, run = s.g * D2;
+    Prof pr{p};
+    pr.begin("total", x.sc);
+    pr.begin("pack", x.sc);
+    std::vector<CopyJob> jobs;
+    const long long offs[3] = {p->off_recvQ, p->off_recvK, p->off_recvV};
+    for (int r = 0; r < p->Psrc; ++r) {
+        const void *xs[3] = {x.ptr.q[r], x.ptr.k[r], x.ptr.v[r]};
+        const long long n = p->len[r];
+        for (int t = 0; t < 3; ++t)
+            for (int kh = 0; kh < s.G_h; ++kh)
+                for (int q = 0; q < p->P; ++q) {
+                    const int nreal = real_heads(p, s, q, kh);
+                    if (nreal == 0) continue;
+                    const uint8_t *src = reinterpret_cast<const uint8_t *>(xs[t]) + (q * p->h + kh * s.g) * D2;
+                    uint8_t *wq = resolve(x, q, BUF_WS, offs[t]);
+                    CopyJob j{};
+                    j.count[0] = j.count[1] = 1;
+                    j.count[2] = p->sh.B;
+                    j.src_stride[2] = n * H * D2; j.src_stride[3] = H * D2;
+                    j.dst_stride[3] = run;
+                    j.run_bytes = nreal * D2;
+                    if (t == 0) {   // Q: chunk c of this source's tokens -> stage (kh, c) of owner q
+                        for (int c = 0; c < s.C; ++c) {
+                            const long long L = Lsrc(p, s, r, c);
+                            if (L == 0) continue;
+                            CopyJob jc = j;
+                            jc.src = src + clo(p, s, r, c) * H * D2;
+                            jc.dst = wq + idx_qo(p, s, kh, c, 0, r) * 2;
+                            jc.count[3] = L;
+                            jc.dst_stride[2] = Lstage(p, s, c) * run;
+                            jobs.push_back(jc);
+                        }
+                    } else {        // K / V: all of this source's tokens -> owner q's full-sequence region
+                        j.src = src;
+                        j.dst = wq + idx_kv(p, s, kh, 0, r) * 2;
+                        j.count[3] = n;
+                        j.dst_stride[2] = (long long)p->sh.S * run;
+                        jobs.push_back(j);
+                    }
+                }
+    }
+    SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sc, &p->copy_launches));
+    pr.end("pack", x.sc);
+    // stages alternate between two streams so stage k+1 fills stage k's wave tail (as in execute())
+    if (!p->sc_alt) SPA_CHECK_CUDA(cudaStreamCreateWithFlags(&p->sc_alt, cudaStreamNonBlocking));
+    cudaEvent_t ev_pack = p->sync_ev[1], ev_alt = p->sync_ev[2];
+    SPA_CHECK_CUDA(cudaEventRecord(ev_pack, x.sc));
+    SPA_CHECK_CUDA(cudaStreamWaitEvent(p->sc_alt, ev_pack, 0));
+    for (int k = 0; k < N; ++k) {
+        const int kh = k / s.C, c = k % s.C;
+        const long long Lst = Lstage(p, s, c);
+        const std::string an = "attn" + std::to_string(k);
+        cudaStream_t st = (k & 1) ? p->sc_alt : x.sc;
+        pr.begin(an, st);
+        for (int r = 0; r < p->P; ++r) {   // owner r
+            const int nreal = real_heads(p, s, r, kh);
+            if (nreal == 0) continue;
+            uint8_t *ws = resolve(x, r, BUF_WS, 0);
+            AttnProblem a{};
+            a.q = ws + p->off_recvQ + base_stage(p, s, kh, c) * 2;
+            a.k = ws + p->off_recvK + idx_kv(p, s, kh, 0, 0) * 2;
+            a.v = ws + p->off_recvV + idx_kv(p, s, kh, 0, 0) * 2;
+            a.o = ws + p->off_O;   // unused (scattered output)
+            a.B = p->sh.B; a.Sq = (int)Lst; a.Skv = p->sh.S; a.n_heads = nreal; a.D = p->sh.D;
+            a.kv_len = p->kv_len;
+            a.q_tok_stride = a.kv_tok_stride = (long long)s.g * p->sh.D;
+            a.q_batch_stride = Lst * s.g * p->sh.D;
+            a.kv_batch_stride = (long long)p->sh.S * s.g * p->sh.D;
+            a.o_tok_stride = H * p->sh.D;
+            a.o_batch_stride = 0;
+            a.n_dst = p->Psrc;
+            for (int q = 0; q < p->Psrc; ++q) {
+                a.row_begin[q] = (int)src_prefix(p, s, c, q);
+                a.dst[q] = reinterpret_cast<uint8_t *>(x.ptr.out[q]) +
+                           ((clo(p, s, q, c) * H) + (long long)r * p->h + (long long)kh * s.g) * D2;
+                a.dst_batch_stride[q] = (long long)p->len[q] * H * p->sh.D;
+            }
+            a.row_begin[p->Psrc] = (int)Lst;
+            SPA_CHECK_CUDA(launch_attention(a, st));
+            ++p->attn_launches;
+        }
+        pr.end(an, st);
+    }
+    SPA_CHECK_CUDA(cudaEventRecord(ev_alt, p->sc_alt));
+    SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_alt, 0));
+    pr.end("total", x.sc);
+    finish_profile(p, pr);
+    return SPA_OK;
+}
+
 // The whole call: single-rank fast path, else the staged pipeline.
 spa_status execute(Exec &x) {
     spa_plan *p = x.p;
@@ -478,6 +578,7 @@ spa_status execute(Exec &x) {
     const Split &s = *x.s;
     const int N = s.n();
     SPA_TRY(ensure_events(p, 4 + 3 * (size_t)N, p->profile ? 8 + 6 * (size_t)N : 0));
+    if (p->direct && p->P > 1 && x.has_attn && x.has_pack && x.has_out) return execute_direct(x);
     Prof pr{p};
     if (p->P == 1) {
         // one rank owns everything: attention straight on the caller's [B,S,H,D] buffers
@@ -930,6 +1031,13 @@ spa_status spa_plan_set_option(spa_plan *plan, int option, int value) {
         case SPA_OPT_PROFILE: plan->profile = value != 0; break;
         case SPA_OPT_SKIP_COMM: plan->skip_comm = value != 0; break;
         case SPA_OPT_COPROC_BUSY: plan->coproc_busy = value != 0; break;
+        case SPA_OPT_DIRECT:
+            if (value && plan->comm->kind == KIND_NCCL)
+                return fail(SPA_ERR_UNSUPPORTED, "direct transport: NVLink windows not built yet (loopback only)");
+            if (value && (plan->ring || plan->Psrc > kMaxDst))
+                return fail(SPA_ERR_UNSUPPORTED, "direct transport: PipeSP / Ulysses / Aco plans with <= 16 sources");
+            plan->direct = value != 0;
+            break;
         default: return fail(SPA_ERR_INVALID, "unknown option");
     }
     return SPA_OK;

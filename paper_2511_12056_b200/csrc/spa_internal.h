@@ -7,6 +7,8 @@
 
 namespace spa {
 
+constexpr int kMaxDst = 16;   // ranks one attention launch can scatter its output rows to
+
 // Attention problem for one launch (a head group of one stage, or a whole single-GPU layer).
 // Element (b, s, j, d) of q is at q + b*q_batch_stride + s*q_tok_stride + j*D + d (elements).
 struct AttnProblem {
@@ -19,6 +21,13 @@ struct AttnProblem {
     const int32_t *kv_len = nullptr;   // key padding: device int32 [B], keys t >= kv_len[b] masked (NULL: none)
     void *o32 = nullptr;               // non-NULL: fp32 output instead of o (same element strides)
     float *lse = nullptr;              // non-NULL: per-row log-sum-exp, [B][Sq][n_heads] contiguous
+    // Scattered output (direct transport): n_dst > 0 -> query rows [row_begin[i], row_begin[i+1]) go
+    // to dst[i] + b*dst_batch_stride[i] + (s - row_begin[i])*o_tok_stride + j*D (o is unused); row_begin has
+    // n_dst + 1 entries.
+    int n_dst = 0;
+    int row_begin[kMaxDst + 1] = {};
+    void *dst[kMaxDst] = {};
+    long long dst_batch_stride[kMaxDst] = {};
 };
 
 // Kernel-side arguments (tensor maps travel separately as __grid_constant__ parameters).
@@ -31,6 +40,10 @@ struct AttnArgs {
     float *O32;              // NULL or fp32 output
     float *lse;              // NULL or [B][Sq][lse_heads]
     int lse_heads;
+    int n_dst;               // > 0: scattered output (see AttnProblem)
+    int row_begin[kMaxDst + 1];
+    __nv_bfloat16 *dst[kMaxDst];
+    long long dst_batch_stride[kMaxDst];
 };
 
 // out[b, s, j, :] = sum_i w_i O_i[b, s, j, :] / sum_i w_i, w_i = exp(lse_i - max_i lse_i), over n partial results

@@ -20,10 +20,10 @@ __all__ = [
     "spa_ring_attention", "spa_ring_attention_local", "spa_attention_host",
     "spa_reshard_seq_to_head", "spa_reshard_head_to_seq", "spa_reshard_seq_to_head_local",
     "spa_reshard_head_to_seq_local", "spa_pad_heads", "attention", "BUF_Q", "BUF_K", "BUF_V", "BUF_OUT",
-    "BUF_WS", "SPA_OPT_PROFILE", "SPA_OPT_SKIP_COMM", "SPA_OPT_COPROC_BUSY",
+    "BUF_WS", "SPA_OPT_PROFILE", "SPA_OPT_SKIP_COMM", "SPA_OPT_COPROC_BUSY", "SPA_OPT_DIRECT",
 ]
 
-SPA_OPT_PROFILE, SPA_OPT_SKIP_COMM, SPA_OPT_COPROC_BUSY = 1, 2, 3
+SPA_OPT_PROFILE, SPA_OPT_SKIP_COMM, SPA_OPT_COPROC_BUSY, SPA_OPT_DIRECT = 1, 2, 3, 4
 BUF_Q, BUF_K, BUF_V, BUF_OUT, BUF_WS = 0, 1, 2, 3, 4
 HEADER = os.path.join(os.path.dirname(_build.HERE), "include", "spa.h")
 

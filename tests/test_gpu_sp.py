@@ -194,3 +194,27 @@ def test_two_plans_on_two_streams_concurrently():
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(outs_a, 1).view(torch.int16), single.view(torch.int16))
     assert torch.equal(torch.cat(outs_b, 1).view(torch.int16), single2.view(torch.int16))
+
+
+@pytest.mark.parametrize("P,S,H,stages,pad,n_src,masked", [
+    (2, 2 * 200, 4, 2, False, 0, False), (4, 4 * 150 + 3, 8, 4, False, 0, True), (8, 8 * 93, 24, 24, False, 0, False),
+    (7, 7 * 64 + 5, 24, 1, True, 0, False), (8, 7 * 90 + 4, 24, 3, False, 7, False), (3, 3 * 100, 6, 6, False, 0, True),
+])
+def test_direct_transport_bit_identical(P, S, H, stages, pad, n_src, masked):
+    """SPA_OPT_DIRECT (SURVEY f1 data path on loopback): pack into the owners' receive regions, attention epilogue
+    into the sources' outputs -- same bits as the single-GPU kernel (and so as the staged exchange)."""
+    B, D = 2, 128
+    q, k, v = U.qkv(B, S, H, D, seed=S + P)
+    kv_len = torch.tensor([S - 33, S // 2], dtype=torch.int32, device="cuda") if masked else None
+    single = spa.attention(q, k, v, kv_len=kv_len)
+    plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=stages, n_src=n_src, pad_heads=pad)
+    plan.set_option(spa.SPA_OPT_DIRECT, 1)
+    if masked:
+        plan.set_kv_len(kv_len)
+    n = n_src or P
+    qs, ks, vs = _shards(q, n), _shards(k, n), _shards(v, n)
+    outs = [torch.full_like(t, float("nan")) for t in qs]
+    call = spa.spa_aco_attention_local if n_src else spa.spa_pipesp_attention_local
+    call(plan, qs, ks, vs, outs, plan.workspace())
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(outs, dim=1).view(torch.int16), single.view(torch.int16))

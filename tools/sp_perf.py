@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--aco", type=int, default=0, help="n_src for an Aco plan (0 = PipeSP)")
     ap.add_argument("--ring", action="store_true", help="Ring-Attention plan instead of PipeSP")
     ap.add_argument("--pad", action="store_true", help="head padding when H % P != 0 (PAPER.md:196-199)")
+    ap.add_argument("--direct", action="store_true", help="direct transport (SPA_OPT_DIRECT, loopback model of f1)")
     args = ap.parse_args()
     w = synthgen.WORKLOADS[args.workload]
     B, S, H, D, P = w.B, w.S, w.H, w.D, args.P
@@ -73,6 +74,8 @@ def main():
         return
     for st in [int(x) for x in args.stages.split(",")]:
         plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=st, n_src=args.aco, pad_heads=args.pad)
+        if args.direct:
+            plan.set_option(spa.SPA_OPT_DIRECT, 1)
         ws = plan.workspace()
         call = spa.spa_aco_attention_local if args.aco else spa.spa_pipesp_attention_local
         for _ in range(2):
