@@ -41,9 +41,11 @@ def _sample(S, P, n=48, seed=0):
     return torch.tensor(rows)
 
 
-def _pipesp(P, q, k, v, stages):
+def _pipesp(P, q, k, v, stages, direct=False):
     B, S, H, D = q.shape
     plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=stages)
+    if direct:
+        plan.set_option(spa.SPA_OPT_DIRECT, 1)
     S_l = S // P
     shards = [[x[:, r * S_l:(r + 1) * S_l].contiguous() for r in range(P)] for x in (q, k, v)]
     outs = [torch.empty_like(t) for t in shards[0]]
@@ -81,6 +83,8 @@ def test_720p_p8_pipesp_stages_bit_identical():
         out = _pipesp(8, q, k, v, st)
         assert torch.equal(out.view(torch.int16), single.view(torch.int16)), st
         del out
+    out = _pipesp(8, q, k, v, 3, direct=True)   # SPA_OPT_DIRECT: the f1 data path (loopback model)
+    assert torch.equal(out.view(torch.int16), single.view(torch.int16))
 
 
 def test_aco_720p_6_plus_2():
