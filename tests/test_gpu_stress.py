@@ -1,6 +1,7 @@
 """Randomised and numerically hard GPU cases through the C ABI (seeded, reproducible).
 
-* random plan shapes (P, H, D, B, S/P, stage count, head padding, key padding) -- PipeSP over P virtual ranks
+* random plan shapes (P, H, D, B, S -- also not divisible by P --, stage count, head padding, key padding,
+  staged or direct transport) -- PipeSP over P virtual ranks
   must give the same bits as the single-GPU kernel and stay within the north-star tolerance of the fp64
   oracle (R18/R19);
 * large score ranges (Q scaled by powers of two, exact in bf16) that make the running max move often and by
@@ -19,8 +20,13 @@ pytestmark = [pytest.mark.gpu, pytest.mark.timeout(1200)]
 
 
 def _shards(x, n):
-    S_l = x.shape[1] // n
-    return [x[:, r * S_l:(r + 1) * S_l].contiguous() for r in range(n)]
+    """sequence shards, uneven (first S % n ranks one token longer) when n does not divide S"""
+    S, out, t = x.shape[1], [], 0
+    for r in range(n):
+        ln = S // n + (1 if r < S % n else 0)
+        out.append(x[:, t:t + ln].contiguous())
+        t += ln
+    return out
 
 
 def _oracle(q, k, v, kv_len=None):
@@ -47,10 +53,11 @@ def _case(seed):
     return P, H, D, B, S_l, max(stages, 1), pad, masked, rng
 
 
-@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("seed", range(40))
 def test_random_plans_bit_identical_and_within_tolerance(seed):
     P, H, D, B, S_l, stages, pad, masked, rng = _case(seed)
-    S = S_l * P
+    S = S_l * P + int(rng.integers(0, P))      # uneven shards (R9) in about half the cases
+    direct = bool(rng.integers(0, 2))          # SPA_OPT_DIRECT (f1 data path, loopback model)
     q, k, v = U.qkv(B, S, H, D, seed=1000 + seed)
     kv_len = None
     if masked:
@@ -59,12 +66,14 @@ def test_random_plans_bit_identical_and_within_tolerance(seed):
     plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=stages, pad_heads=pad)
     if kv_len is not None:
         plan.set_kv_len(kv_len)
+    if direct:
+        plan.set_option(spa.SPA_OPT_DIRECT, 1)
     qs, ks, vs = _shards(q, P), _shards(k, P), _shards(v, P)
     outs = [torch.full_like(t, float("nan")) for t in qs]
     spa.spa_pipesp_attention_local(plan, qs, ks, vs, outs, plan.workspace())
     torch.cuda.synchronize()
     out = torch.cat(outs, dim=1)
-    assert torch.equal(out.view(torch.int16), single.view(torch.int16)), (P, H, D, B, S_l, stages, pad, masked)
+    assert torch.equal(out.view(torch.int16), single.view(torch.int16)), (P, H, D, B, S, stages, pad, masked, direct)
     U.assert_close(out, _oracle(q, k, v, None if kv_len is None else kv_len.tolist()))
 
 
