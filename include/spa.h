@@ -191,7 +191,8 @@ spa_status spa_attention_host(spa_plan *plan, const void *q, const void *k, cons
  * the comm stream (double-buffered, NCCL send/recv) while the previous block is computed; each step writes
  * an fp32 partial result and its per-row log-sum-exp into ws, and a merge kernel combines the P partials
  * (softmax over the union of the blocks).  Not bit-identical to the Ulysses path (a different summation
- * order), within the same tolerance of the fp64 definition.  Key-padding masks: SPA_ERR_UNSUPPORTED. */
+ * order), within the same tolerance of the fp64 definition.  Key-padding masks (spa_plan_set_kv_len) apply by
+ * global key position to every block (a wholly masked block contributes lse = -inf). */
 spa_status spa_ring_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out, void *ws,
                               void *stream);
 spa_status spa_ring_attention_local(spa_plan *plan, const void *const q[], const void *const k[],

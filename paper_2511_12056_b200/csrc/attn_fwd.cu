@@ -218,8 +218,8 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1)
     // key-padding mask (Alg. 1 attention_mask; R20): keys t >= kv_len[b] take no
     // part; tiles wholly beyond it are never loaded.  Both CTAs of a cluster share b, hence n_kv.
     int Skv_b = args.Skv;
-    if (args.kv_len) {
-        const int L = __ldg(args.kv_len + b);
+    if (args.kv_len) {   // key t of this launch is global key t + kv_offset (ring blocks)
+        const int L = __ldg(args.kv_len + b) - args.kv_offset;
         Skv_b = L < 0 ? 0 : (L < Skv_b ? L : Skv_b);
     }
     const int n_kv = (Skv_b + BN - 1) / BN;   // 0: every row of this batch entry is 0
@@ -680,6 +680,7 @@ cudaError_t launch_d(const AttnProblem &p, cudaStream_t st) {
     a.Skv = p.Skv;
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
     a.kv_len = p.kv_len;
+    a.kv_offset = p.kv_offset;
     a.O32 = reinterpret_cast<float *>(p.o32);
     a.lse = p.lse;
     a.lse_heads = p.n_heads;

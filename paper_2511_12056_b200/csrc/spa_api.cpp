@@ -1127,14 +1127,15 @@ spa_status spa_aco_attention_local(spa_plan *plan, const void *const q[], const 
 // travels the ring r-1 -> r -> r+1 on the comm stream while the previous block is being computed (double-buffered
 // receive slots); every step writes an fp32 partial O and its per-row lse, and lse_merge combines the P partials.
 static AttnProblem ring_problem(const spa_plan *p, const void *q, const void *k, const void *v, float *o32,
-                                float *lse) {
+                                float *lse, int kv_src = 0) {
     AttnProblem a{};
     const long long tok = (long long)p->sh.H * p->sh.D;
     a.q = q; a.k = k; a.v = v; a.o = nullptr; a.o32 = o32; a.lse = lse;
     a.B = p->sh.B; a.Sq = a.Skv = p->S_l; a.n_heads = p->sh.H; a.D = p->sh.D;
     a.q_tok_stride = a.kv_tok_stride = a.o_tok_stride = tok;
     a.q_batch_stride = a.kv_batch_stride = a.o_batch_stride = (long long)p->S_l * tok;
-    a.kv_len = nullptr;   // a key-padding mask is global-position based: not supported on ring plans
+    a.kv_len = p->kv_len;   // key-padding mask by global position: this block's keys start at kv_src * S_l
+    a.kv_offset = kv_src * p->S_l;
     return a;
 }
 
@@ -1142,8 +1143,11 @@ static spa_status ring_call(spa_plan *p, int n, const void *const q[], const voi
                             void *const out[], void *ws, void *stream, bool local) {
     if (!p) return fail(SPA_ERR_INVALID, "plan is NULL");
     if (!p->ring) return fail(SPA_ERR_INVALID, "not a ring plan (shape.ring = 1)");
-    if (p->kv_len) return fail(SPA_ERR_UNSUPPORTED, "key-padding masks are not supported on ring plans");
-    if (p->U > 1) return usp_call(p, q, k, v, out, ws, stream, local);
+    if (p->U > 1) {
+        // the ring runs over the Ulysses groups, whose token blocks are contiguous in the global sequence
+        SPA_TRY(spa_plan_set_kv_len(p->ring_plan, p->kv_len));
+        return usp_call(p, q, k, v, out, ws, stream, local);
+    }
     Exec x{};
     SPA_TRY(prepare(p, x, ws, stream, local));
     for (int i = 0; i < n; ++i) {
@@ -1177,7 +1181,7 @@ static spa_status ring_call(spa_plan *p, int n, const void *const q[], const voi
         for (int r = 0; r < P; ++r) {
             for (int t = 0; t < P; ++t) {
                 const int src = ((r - t) % P + P) % P;
-                AttnProblem a = ring_problem(p, q[r], k[src], v[src], parts(r) + t * p->E_loc, lses(r) + t * rows);
+                AttnProblem a = ring_problem(p, q[r], k[src], v[src], parts(r) + t * p->E_loc, lses(r) + t * rows, src);
                 SPA_CHECK_CUDA(launch_attention(a, sc));
                 ++p->attn_launches;
             }
@@ -1213,7 +1217,7 @@ static spa_status ring_call(spa_plan *p, int n, const void *const q[], const voi
             SPA_CHECK_CUDA(cudaEventRecord(comm[t], sm));
         }
         if (t >= 1) SPA_CHECK_CUDA(cudaStreamWaitEvent(sc, comm[t - 1], 0));
-        AttnProblem a = ring_problem(p, q[0], ck, cv, parts(r) + t * p->E_loc, lses(r) + t * rows);
+        AttnProblem a = ring_problem(p, q[0], ck, cv, parts(r) + t * p->E_loc, lses(r) + t * rows, (r - t + P) % P);
         SPA_CHECK_CUDA(launch_attention(a, sc));
         ++p->attn_launches;
         SPA_CHECK_CUDA(cudaEventRecord(comp[t], sc));

@@ -19,6 +19,8 @@ struct AttnProblem {
     long long kv_tok_stride, kv_batch_stride;
     long long o_tok_stride, o_batch_stride;
     const int32_t *kv_len = nullptr;   // key padding: device int32 [B], keys t >= kv_len[b] masked (NULL: none)
+    int kv_offset = 0;                 // global position of this launch's key 0 (ring blocks): t masked iff
+                                       // t + kv_offset >= kv_len[b]
     void *o32 = nullptr;               // non-NULL: fp32 output instead of o (same element strides)
     float *lse = nullptr;              // non-NULL: per-row log-sum-exp, [B][Sq][n_heads] contiguous
     // Scattered output (direct transport): n_dst > 0 -> query rows [row_begin[i], row_begin[i+1]) go
@@ -37,6 +39,7 @@ struct AttnArgs {
     int Sq, Skv;
     float scale_log2;
     const int32_t *kv_len;   // NULL or device [B]
+    int kv_offset;
     float *O32;              // NULL or fp32 output
     float *lse;              // NULL or [B][Sq][lse_heads]
     int lse_heads;

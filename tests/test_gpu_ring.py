@@ -5,6 +5,8 @@ Ulysses cannot split."""
 import pytest
 import torch
 
+import oracle
+
 from paper_2511_12056_b200 import spa
 from tests import gpu_util as U
 
@@ -76,3 +78,21 @@ def test_usp_hybrid_vs_oracle(P, Ud, H, D):
     assert not torch.isnan(out).any()
     U.assert_close(out, U.oracle_mha(q, k, v))
     assert torch.equal(out.view(torch.int16), _usp(P, Ud, q, k, v).view(torch.int16))
+
+
+@pytest.mark.parametrize("P,Ud", [(4, 1), (8, 1), (4, 2), (8, 4)])
+def test_ring_and_usp_with_key_padding(P, Ud):
+    """Key-padding masks on ring plans apply by global key position to every ring block (blocks wholly past
+    kv_len contribute nothing: lse = -inf)."""
+    B, S, H, D = 2, 96 * P, 2 * Ud, 96
+    q, k, v = U.qkv(B, S, H, D, seed=P * 7 + Ud)
+    kv_len = torch.tensor([S - 97, S // 3], dtype=torch.int32, device="cuda")
+    plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, ring=True, ulysses=Ud)
+    plan.set_kv_len(kv_len)
+    qs, ks, vs = _shards(q, P), _shards(k, P), _shards(v, P)
+    outs = [torch.full_like(t, float("nan")) for t in qs]
+    spa.spa_ring_attention_local(plan, qs, ks, vs, outs, plan.workspace())
+    torch.cuda.synchronize()
+    Q, K, V = (t.detach().cpu().double().numpy() for t in (q, k, v))
+    ref = oracle.mha_unsharded(Q, K, V, key_valid=oracle.key_valid_from_lengths(kv_len.tolist(), S))
+    U.assert_close(torch.cat(outs, dim=1), ref)
