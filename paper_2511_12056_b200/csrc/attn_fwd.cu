@@ -145,11 +145,12 @@ struct Cfg {
     static_assert(O_COL + D <= TMEM_COLS, "TMEM budget");
     static constexpr int OCHUNKS = D / 16;               // epilogue: 16-column chunks, chunk c by group c % NG
     // exp2 split: key pairs with (key & 15) >= POLY_FROM use the FMA-pipe polynomial, the rest MUFU.EX2
-    // (POLY_FROM = 12: a quarter of the keys on the FMA pipe; 16: none).
+    // (POLY_FROM = 12: a quarter of the keys on the FMA pipe; 14: an eighth; 16: none).
 #ifdef SPA_POLY_FROM
     static constexpr int POLY_FROM = SPA_POLY_FROM;
 #else
-    static constexpr int POLY_FROM = 12;
+    // sweeps (profiles/r01_v5_experiments): 1/4 on the FMA pipe is best at D=128, 1/8 at D=96 (+~2 %, noisy)
+    static constexpr int POLY_FROM = (D == 96) ? 14 : 12;
 #endif
     static_assert(SMEM_BYTES + XCH_BYTES <= 227 * 1024, "shared memory");
     static_assert(NS <= 16, "barrier block");
