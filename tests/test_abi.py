@@ -202,3 +202,20 @@ def test_messages_stay_inside_workspace():
                     assert 0 <= m.off and m.off + m.bytes <= nb and m.off % 16 == 0 and m.bytes % 64 == 0
             a = plans[r].describe_attention(k, r)
             assert a.q_off % 16 == 0 and a.o_off % 16 == 0 and a.Skv == 64
+
+
+def test_plain_c_client(tmp_path):
+    """The boundary is a C ABI: a plain C program (tests/c_abi/abi_smoke.c) compiled with gcc against
+    include/spa.h and libspa.so creates plans and reads their descriptions without Python or torch."""
+    import os
+    import subprocess
+    from paper_2511_12056_b200 import _build
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = _build.build()
+    exe = str(tmp_path / "abi_smoke")
+    subprocess.check_call(["gcc", "-std=c11", "-O1", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "tests", "c_abi", "abi_smoke.c"), lib, "-o", exe,
+                           f"-Wl,-rpath,{os.path.dirname(lib)}"])
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0, out.stderr
+    assert "c abi ok" in out.stdout
