@@ -98,7 +98,8 @@ typedef struct {
     int ring;       /* 0: Ulysses / PipeSP / Aco plan.  1: Ring-Attention plan ("switch ... from
                        Ulysses to Ring-Attention ... avoiding the overhead of padding"; R21): every
                        rank keeps all H heads of its sequence shard, only S % nranks == 0 is required (any H);
-                       use spa_ring_attention*.  stages, n_src and pad_heads must be 0 / 1 / 0. */
+                       use spa_ring_attention*.  stages must be 1 and pad_heads 0 (else SPA_ERR_INVALID);
+                       n_src 0 or nranks (else SPA_ERR_SHAPE). */
     int ulysses;    /* ring plans only: Ulysses degree U of the USP hybrid ("flexible configuration
                        of both the Ulysses degree and the Ring-Attention degree"); 0 or 1 = pure Ring.  U > 1:
                        U | nranks and U | H; ranks [rho*U, rho*U+U) form Ulysses group rho, the R = nranks/U
@@ -164,7 +165,8 @@ spa_status spa_ulysses_attention(spa_plan *plan, const void *q, const void *k, c
 spa_status spa_pipesp_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out,
                                 void *ws, void *stream);
 /* Aco: plan with 0 < n_src < nranks.  Ranks < n_src pass their shards;
- * co-processor ranks (>= n_src) pass NULL for q, k, v, out. */
+ * co-processor ranks (>= n_src) pass NULL for q, k, v, out.  A plan without co-processor ranks
+ * (n_src == 0 or nranks, i.e. N_decode = 0) runs PipeSP on all ranks. */
 spa_status spa_aco_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out,
                              void *ws, void *stream);
 

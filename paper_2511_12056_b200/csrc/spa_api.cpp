@@ -116,6 +116,7 @@ struct spa_plan {
     std::vector<cudaEvent_t> prof_ev;  // timing events
     spa_profile last{};
     bool have_profile = false;
+    int prof_stages = 0;   // stages the last profiled call executed (spa_profile.n_stages)
     std::map<std::string, int> prof_idx;
     int attn_launches = 0, copy_launches = 0;
     cudaStream_t sc_alt = nullptr;  // second compute stream: odd stages, so stage k+1 fills stage k's wave tail
@@ -453,9 +454,10 @@ spa_status run_unpack(Exec &x) {
     return SPA_OK;
 }
 
-void finish_profile(spa_plan *p, const Prof &pr) {
+void finish_profile(spa_plan *p, const Prof &pr, int n_stages) {
     p->have_profile = false;
     if (!p->profile) return;
+    p->prof_stages = n_stages;
     p->last = spa_profile{};
     p->last.n_stages = 0;
     p->prof_idx.clear();
@@ -566,7 +568,7 @@ spa_status execute_direct(Exec &x) {
     SPA_CHECK_CUDA(cudaEventRecord(ev_alt, p->sc_alt));
     SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_alt, 0));
     pr.end("total", x.sc);
-    finish_profile(p, pr);
+    finish_profile(p, pr, N);
     return SPA_OK;
 }
 
@@ -601,7 +603,7 @@ spa_status execute(Exec &x) {
             SPA_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, x.sc));
         }
         pr.end("total", x.sc);
-        finish_profile(p, pr);
+        finish_profile(p, pr, 1);
         return SPA_OK;
     }
     SPA_TRY(ensure_stream(p->comm));
@@ -672,7 +674,7 @@ spa_status execute(Exec &x) {
     // make the comm stream's tail visible to later work on the caller's stream
     SPA_CHECK_CUDA(cudaEventRecord(ev_done, x.sm));
     SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_done, 0));
-    finish_profile(p, pr);
+    finish_profile(p, pr, x.has_attn ? N : 1);
     return SPA_OK;
 }
 
@@ -771,6 +773,14 @@ static spa_status usp_call(spa_plan *p, const void *const q[], const void *const
         SPA_TRY(check_ptr(q[i], "q")); SPA_TRY(check_ptr(k[i], "k"));
         SPA_TRY(check_ptr(v[i], "v")); SPA_TRY(check_ptr(out[i], "out"));
     }
+    SPA_TRY(ensure_events(p, 0, p->profile ? 2 : 0));
+    Prof pr{p};
+    pr.begin("total", reinterpret_cast<cudaStream_t>(stream));
+    auto done = [&]() {
+        pr.end("total", reinterpret_cast<cudaStream_t>(stream));
+        finish_profile(p, pr, 1);   // attn_ms[0] = the ring sub-plan's call (spa_plan_last_profile)
+        return SPA_OK;
+    };
     uint8_t *w = reinterpret_cast<uint8_t *>(ws);
     uint8_t *sub_ws = w + p->off_parts;
     auto head = [&](int i, int t) { return w + ((long long)i * 4 + t) * p->E_loc * 2; };   // t: 0 Q 1 K 2 V 3 O
@@ -778,7 +788,8 @@ static spa_status usp_call(spa_plan *p, const void *const q[], const void *const
     if (!local) {
         for (int t = 0; t < 3; ++t) SPA_TRY(spa_reshard_seq_to_head(p->uly_plan, in[t][0], head(0, t), sub_ws, stream));
         SPA_TRY(spa_ring_attention(p->ring_plan, head(0, 0), head(0, 1), head(0, 2), head(0, 3), sub_ws, stream));
-        return spa_reshard_head_to_seq(p->uly_plan, head(0, 3), out[0], sub_ws, stream);
+        SPA_TRY(spa_reshard_head_to_seq(p->uly_plan, head(0, 3), out[0], sub_ws, stream));
+        return done();
     }
     std::vector<const void *> xs(U);
     std::vector<void *> hs(U);
@@ -802,7 +813,7 @@ static spa_status usp_call(spa_plan *p, const void *const q[], const void *const
         std::vector<const void *> hc(hs.begin(), hs.end());
         SPA_TRY(spa_reshard_head_to_seq_local(p->uly_plan, hc.data(), os.data(), sub_ws, stream));
     }
-    return SPA_OK;
+    return done();
 }
 
 // ==================================================================== C ABI
@@ -937,6 +948,8 @@ spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *sha
     if (s.pad_heads != 0 && s.pad_heads != 1) return fail(SPA_ERR_INVALID, "pad_heads must be 0 or 1");
     if (s.ring != 0 && s.ring != 1) return fail(SPA_ERR_INVALID, "ring must be 0 or 1");
     if (s.ulysses < 0 || (!s.ring && s.ulysses > 1)) return fail(SPA_ERR_INVALID, "ulysses degree needs ring = 1");
+    if (s.ring && (s.stages != 1 || s.pad_heads != 0))
+        return fail(SPA_ERR_INVALID, "ring / USP plans take stages = 1 and pad_heads = 0");
     if (s.ring && s.ulysses > 1) return create_usp_plan(plan, comm, s);
     if (s.ring) {
         // Ring attention: every rank keeps all heads; only S % P matters.
@@ -1027,6 +1040,10 @@ spa_status spa_plan_destroy(spa_plan *plan) {
 
 spa_status spa_plan_set_option(spa_plan *plan, int option, int value) {
     if (!plan) return fail(SPA_ERR_INVALID, "plan is NULL");
+    if (plan->U > 1 && (option == SPA_OPT_PROFILE || option == SPA_OPT_SKIP_COMM)) {   // USP: the sub-plans too
+        SPA_TRY(spa_plan_set_option(plan->uly_plan, option, value));
+        SPA_TRY(spa_plan_set_option(plan->ring_plan, option, value));
+    }
     switch (option) {
         case SPA_OPT_PROFILE: plan->profile = value != 0; break;
         case SPA_OPT_SKIP_COMM: plan->skip_comm = value != 0; break;
@@ -1061,7 +1078,7 @@ spa_status spa_plan_last_profile(spa_plan *plan, spa_profile *out) {
         if (err != cudaSuccess) return fail(SPA_ERR_CUDA, std::string("profile: ") + cudaGetErrorString(err));
         return SPA_OK;
     };
-    const int N = plan->P == 1 ? 1 : plan->split.n();
+    const int N = plan->prof_stages;
     r.n_stages = N;
     SPA_TRY(span("total", &r.total_ms));
     SPA_TRY(span("pack", &r.pack_ms));
@@ -1073,6 +1090,13 @@ spa_status spa_plan_last_profile(spa_plan *plan, spa_profile *out) {
     }
     r.attn_launches = plan->attn_launches;
     r.copy_launches = plan->copy_launches;
+    if (plan->U > 1 && plan->ring_plan->have_profile) {   // USP: the ring sub-plan's (last) call is the attention
+        spa_profile rp{};
+        SPA_TRY(spa_plan_last_profile(plan->ring_plan, &rp));
+        r.attn_ms[0] = rp.total_ms;
+        r.attn_launches = rp.attn_launches;
+        r.copy_launches = rp.copy_launches;
+    }
     *out = r;
     return SPA_OK;
 }
@@ -1090,9 +1114,10 @@ spa_status spa_pipesp_attention(spa_plan *plan, const void *q, const void *k, co
 spa_status spa_aco_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out, void *ws,
                              void *stream) {
     if (!plan) return fail(SPA_ERR_INVALID, "plan is NULL");
-    if (plan->Psrc == plan->P) return fail(SPA_ERR_INVALID, "not an Aco plan (n_src must be < nranks)");
-    if (plan->coproc_busy) return fail(SPA_ERR_BUSY, "co-processor group busy");
     if (plan->ring) return fail(SPA_ERR_INVALID, "ring plan: use spa_ring_attention");
+    // no co-processor ranks (N_decode = 0): Aco is PipeSP on all ranks
+    if (plan->Psrc == plan->P) return attention_call(plan, 1, &q, &k, &v, &out, ws, stream, false, false);
+    if (plan->coproc_busy) return fail(SPA_ERR_BUSY, "co-processor group busy");
     const bool src = plan->comm->kind == KIND_NCCL && is_source(plan, plan->comm->rank);
     if (!src) {
         if (q || k || v || out) return fail(SPA_ERR_INVALID, "co-processor ranks pass NULL q/k/v/out");
@@ -1117,8 +1142,7 @@ spa_status spa_pipesp_attention_local(spa_plan *plan, const void *const q[], con
 spa_status spa_aco_attention_local(spa_plan *plan, const void *const q[], const void *const k[],
                                    const void *const v[], void *const out[], void *ws, void *stream) {
     if (!plan || !q || !k || !v || !out) return fail(SPA_ERR_INVALID, "NULL argument");
-    if (plan->Psrc == plan->P) return fail(SPA_ERR_INVALID, "not an Aco plan (n_src must be < nranks)");
-    if (plan->coproc_busy) return fail(SPA_ERR_BUSY, "co-processor group busy");
+    if (plan->Psrc != plan->P && plan->coproc_busy) return fail(SPA_ERR_BUSY, "co-processor group busy");
     return attention_call(plan, n_local_srcs(plan), q, k, v, out, ws, stream, true, false);
 }
 
@@ -1159,11 +1183,18 @@ static spa_status ring_call(spa_plan *p, int n, const void *const q[], const voi
     const int P = p->P;
     const long long tok = (long long)p->sh.H * p->sh.D;
     cudaStream_t sc = x.sc;
+    SPA_TRY(ensure_events(p, 4 + 2 * (size_t)P, p->profile ? 8 + 4 * (size_t)P : 0));
+    Prof pr{p};
+    pr.begin("total", sc);
     if (P == 1) {   // one block: the plain kernel
         AttnProblem a = ring_problem(p, q[0], k[0], v[0], nullptr, nullptr);
         a.o = out[0]; a.o32 = nullptr;
+        pr.begin("attn0", sc);
         SPA_CHECK_CUDA(launch_attention(a, sc));
+        pr.end("attn0", sc);
         ++p->attn_launches;
+        pr.end("total", sc);
+        finish_profile(p, pr, 1);
         return SPA_OK;
     }
     const long long rows = p->E_loc / p->sh.D;
@@ -1178,21 +1209,27 @@ static spa_status ring_call(spa_plan *p, int n, const void *const q[], const voi
     if (p->comm->kind == KIND_LOOPBACK) {
         // virtual ranks on one GPU: step t of rank r reads rank (r - t) mod P's shard in place (the ring's data
         // movement is the identity here; the arithmetic and the merge are the multi-GPU ones)
-        for (int r = 0; r < P; ++r) {
-            for (int t = 0; t < P; ++t) {
+        for (int t = 0; t < P; ++t) {
+            const std::string an = "attn" + std::to_string(t);
+            pr.begin(an, sc);
+            for (int r = 0; r < P; ++r) {
                 const int src = ((r - t) % P + P) % P;
                 AttnProblem a = ring_problem(p, q[r], k[src], v[src], parts(r) + t * p->E_loc, lses(r) + t * rows, src);
                 SPA_CHECK_CUDA(launch_attention(a, sc));
                 ++p->attn_launches;
             }
-            SPA_TRY(merge(r, out[r]));
+            pr.end(an, sc);
         }
+        pr.begin("unpack", sc);   // the lse merge
+        for (int r = 0; r < P; ++r) SPA_TRY(merge(r, out[r]));
+        pr.end("unpack", sc);
+        pr.end("total", sc);
+        finish_profile(p, pr, P);
         return SPA_OK;
     }
     // NCCL: compute on the caller's stream, K/V blocks around the ring on the comm stream
     SPA_TRY(ensure_stream(p->comm));
     cudaStream_t sm = p->comm->stream;
-    SPA_TRY(ensure_events(p, 4 + 2 * (size_t)P, 0));
     cudaEvent_t *ev = p->sync_ev.data();
     cudaEvent_t ev_entry = ev[0], ev_done = ev[1];
     cudaEvent_t *comp = ev + 4, *comm = ev + 4 + P;
@@ -1208,23 +1245,35 @@ static spa_status ring_call(spa_plan *p, int n, const void *const q[], const voi
         const void *cv = t == 0 ? v[0] : slotV((t - 1) & 1);
         if (t + 1 < P) {   // comm step t: pass the current block on, receive the next one
             if (t >= 1) SPA_CHECK_CUDA(cudaStreamWaitEvent(sm, comp[t - 1], 0));   // slot t%2 was read at step t-1
-            SPA_CHECK_NCCL(ncclGroupStart());
-            SPA_CHECK_NCCL(ncclSend(ck, blk, ncclUint8, next, p->comm->nccl, sm));
-            SPA_CHECK_NCCL(ncclSend(cv, blk, ncclUint8, next, p->comm->nccl, sm));
-            SPA_CHECK_NCCL(ncclRecv(slotK(t & 1), blk, ncclUint8, prev, p->comm->nccl, sm));
-            SPA_CHECK_NCCL(ncclRecv(slotV(t & 1), blk, ncclUint8, prev, p->comm->nccl, sm));
-            SPA_CHECK_NCCL(ncclGroupEnd());
+            const std::string cn = "in" + std::to_string(t);
+            pr.begin(cn, sm);
+            if (!p->skip_comm) {   // SPA_OPT_SKIP_COMM: exposed-comm measurement (slots then hold stale data)
+                SPA_CHECK_NCCL(ncclGroupStart());
+                SPA_CHECK_NCCL(ncclSend(ck, blk, ncclUint8, next, p->comm->nccl, sm));
+                SPA_CHECK_NCCL(ncclSend(cv, blk, ncclUint8, next, p->comm->nccl, sm));
+                SPA_CHECK_NCCL(ncclRecv(slotK(t & 1), blk, ncclUint8, prev, p->comm->nccl, sm));
+                SPA_CHECK_NCCL(ncclRecv(slotV(t & 1), blk, ncclUint8, prev, p->comm->nccl, sm));
+                SPA_CHECK_NCCL(ncclGroupEnd());
+            }
+            pr.end(cn, sm);
             SPA_CHECK_CUDA(cudaEventRecord(comm[t], sm));
         }
         if (t >= 1) SPA_CHECK_CUDA(cudaStreamWaitEvent(sc, comm[t - 1], 0));
         AttnProblem a = ring_problem(p, q[0], ck, cv, parts(r) + t * p->E_loc, lses(r) + t * rows, (r - t + P) % P);
+        const std::string an = "attn" + std::to_string(t);
+        pr.begin(an, sc);
         SPA_CHECK_CUDA(launch_attention(a, sc));
+        pr.end(an, sc);
         ++p->attn_launches;
         SPA_CHECK_CUDA(cudaEventRecord(comp[t], sc));
     }
+    pr.begin("unpack", sc);   // the lse merge
     SPA_TRY(merge(r, out[0]));
+    pr.end("unpack", sc);
     SPA_CHECK_CUDA(cudaEventRecord(ev_done, sm));
     SPA_CHECK_CUDA(cudaStreamWaitEvent(sc, ev_done, 0));
+    pr.end("total", sc);
+    finish_profile(p, pr, P);
     return SPA_OK;
 }
 

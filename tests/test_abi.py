@@ -90,6 +90,10 @@ def test_ring_plan_validation_and_workspace():
     with pytest.raises(spa.SpaError):
         p.describe_messages(0, 0, 1)
     assert spa.Plan(spa.Comm.host(1, 0), B, S, H, D, ring=True).workspace_bytes == 0
+    for kw in (dict(stages=2), dict(pad_heads=True), dict(stages=3, ulysses=2)):   # spa.h: stages 1, pad_heads 0
+        with pytest.raises(spa.SpaError) as e:
+            spa.Plan(spa.Comm.host(P, 0), B, S, 4, D, ring=True, **kw)
+        assert e.value.status == 1, kw
 
 
 def test_usp_plan_validation():

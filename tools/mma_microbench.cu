@@ -1,11 +1,11 @@
 // mma_microbench.cu -- raw tcgen05.mma issue rates on this B200 (design input for attn_fwd.cu).
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2511_12056_b200/csrc tools/mma_microbench.cu -o /tmp/mma_mb
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2511_12056_b200/csrc -I tools tools/mma_microbench.cu -o /tmp/mma_mb
 // One elected thread per CTA issues ITER back-to-back MMAs (random bf16 operands), commit, wait.
 // Prints cycles per MMA instruction and the implied bf16 FLOP/clk/SM, for 1 CTA and for 148 CTAs.
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
-#include "ptx.cuh"
+#include "ptx_cta1.cuh"
 
 using namespace spa;
 

@@ -1,10 +1,10 @@
 // softmax_microbench.cu -- cycles per 128x128 softmax tile (pass 1 max + pass 2 exp/sum/pack/store)
 // from/to TMEM, one thread per row, for several instruction mixes.  Design input for attn_fwd.cu.
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2511_12056_b200/csrc tools/softmax_microbench.cu -o tools/sm_mb.bin
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2511_12056_b200/csrc -I tools tools/softmax_microbench.cu -o tools/sm_mb.bin
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
-#include "ptx.cuh"
+#include "ptx_cta1.cuh"
 
 using namespace spa;
 constexpr int ITER = 256;

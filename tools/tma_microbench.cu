@@ -5,13 +5,13 @@
 //   mode 1: clusters of 2, each CTA loads half of every tile and multicasts it (attn_fwd's scheme)
 // Reports bytes landed in each SM's shared memory per SM clock.  Design input for the attention kernel's
 // structure (how many query rows must share one K/V tile).
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2511_12056_b200/csrc tools/tma_microbench.cu -o tools/tma_mb.bin -lcuda
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2511_12056_b200/csrc -I tools tools/tma_microbench.cu -o tools/tma_mb.bin -lcuda
 #include <cuda.h>
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
 
-#include "ptx.cuh"
+#include "ptx_cta1.cuh"
 
 using namespace spa;
 constexpr int NS = 6;

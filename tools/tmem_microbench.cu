@@ -1,12 +1,12 @@
 // tmem_microbench.cu -- TMEM read throughput of tcgen05.ld.32x32b.x32 per SM sub-partition, as a function of the
 // number of warps per sub-partition and of how many loads are in flight before tcgen05.wait::ld.
 // Design input for the softmax pass structure of attn_fwd.cu (two passes over S read it twice).
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2511_12056_b200/csrc tools/tmem_microbench.cu -o tools/tmem_mb.bin
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2511_12056_b200/csrc -I tools tools/tmem_microbench.cu -o tools/tmem_mb.bin
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
 
-#include "ptx.cuh"
+#include "ptx_cta1.cuh"
 
 using namespace spa;
 constexpr int ITER = 512;
