@@ -1,15 +1,21 @@
 #!/usr/bin/env python
 """Benchmark of the PipeSP attention layer (BASELINE.json metric) -- one JSON line on rank 0.
 
-    python bench.py [--gpus N --steps K --warmup W] [--workload osp480p93f] [--stages N_st]
-    torchrun --nproc-per-node N bench.py --gpus N ...           (one process per GPU, NCCL)
+    python bench.py [--gpus N --steps K --warmup W] [--workload hy544p129f] [--stages N_st]
+    python bench.py --gpus N ...      (N > 1 without torchrun: re-launches itself through
+                                       torch.distributed.run, one process per GPU, NCCL)
+    torchrun --nproc-per-node N bench.py --gpus N ...
     python bench.py --impl reference ...                         (the fp64 CPU oracle arm)
 
 A step = one SP attention layer (all SURVEY §8(a) rows: pack, per-stage input all-to-all,
 tcgen05 attention, per-stage output all-to-all, Psi_g unpack) over one batch of synthetic
-Q/K/V shaped like the named workload, inputs resident in HBM.  Strong scaling: the global
-problem (B, S, H, D) is fixed and split over P = N ranks.  `value` = total attention FLOPs
-(4*B*S^2*H*D) / max-over-ranks step time, in TFLOP/s.
+Q/K/V shaped like the named workload, inputs resident in HBM.  Default workload at every N:
+BASELINE configs[2] (HunyuanVideo-like 1024x576x129, S = 76,032, H = 24, D = 128), the largest
+configuration that fits one GPU's benchmark budget and splits over 1/2/4/8 ranks.  Strong scaling:
+the global problem is fixed and split over P = N ranks.  `value` = total attention FLOPs
+(4*B*S^2*H*D) / max over ranks of the per-rank MEDIAN step time, in TFLOP/s.  With N = 8 the line
+adds the north-star block: configs[3] (720p x 129f, S = 118,800) over N_st in {1,2,3,4,6,8,12,24},
+with exposed all-to-all and a2a GB/s per stage split.
 """
 from __future__ import annotations
 
@@ -35,13 +41,16 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="osp480p93f")
+    ap.add_argument("--workload", default="hy544p129f")
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--stages", type=int, default=0, help="N_st (0 = paper's per-head loop, h stages)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-groups", type=int, default=8, help="head groups of the 1-GPU host-buffer e2e call")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
+    ap.add_argument("--spawn", action="store_true", help="launch through torch.distributed.run even at N=1")
+    ap.add_argument("--north-star", type=int, default=-1,
+                    help="720p N_st sweep block: 1 on, 0 off, -1 (default) on when N == 8")
     return ap.parse_args()
 
 
@@ -192,6 +201,20 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
+NORTH_STAR_STAGES = (1, 2, 3, 4, 6, 8, 12, 24)
+NVLINK_GBS = 900.0   # NVLink 5 per direction per GPU (SURVEY §8(d) overlapped roofline)
+
+
+def _a2a_send_bytes(plan, rank):
+    """Bytes this rank sends to OTHER ranks over all stages (input Q/K/V + output O), from the plan's messages."""
+    n = 0
+    G_h, C, _ = plan.stage_split
+    for k in range(G_h * C):
+        for d in (0, 1):
+            n += sum(m.bytes for m in plan.describe_messages(k, d, rank) if not m.is_recv and m.peer != rank)
+    return n
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -212,29 +235,16 @@ def run_ours(args):
     P = world
     if S % P or H % P:
         raise SystemExit(f"workload {name} does not split over {P} ranks")
-    h, S_l = H // P, S // P
-    stages = args.stages or (h if P > 1 else 1)
+    stages = args.stages or (H // P if P > 1 else 1)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > L2 (126 MB)
 
-    # rank's shard of the global synthetic problem, generated on the device
-    qkv = [synthgen.gen_qkv_shard(0, t, (B, S, H, D), rank * S_l, (rank + 1) * S_l, device=dev) for t in range(3)]
-    out = torch.empty_like(qkv[0])
     if P == 1:
         comm = spa.Comm.loopback(1, local)
     else:
         obj = [spa.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         comm = spa.Comm.nccl(obj[0], P, rank, local)
-    plan = spa.Plan(comm, B, S, H, D, stages=stages)
-    ws = plan.workspace(dev)
-    stream = torch.cuda.current_stream()
-
-    def step(q, k, v, o):
-        if P == 1:
-            spa.spa_pipesp_attention_local(plan, [q], [k], [v], [o], ws, stream)
-        else:
-            spa.spa_pipesp_attention(plan, q, k, v, o, ws, stream)
-
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def barrier():
         torch.cuda.synchronize()
@@ -242,57 +252,81 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        step(*qkv, out)
-    barrier()
+    def max_over_ranks(x):
+        t = torch.tensor([float(x)], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
-    plan.set_option(spa.SPA_OPT_PROFILE, 1)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    attn_ms, attn_launches, copy_launches, a2a_in, a2a_out = [], 0, 0, [], []
-    with ClockSampler(local) as clk:
+    def make(workload, n_st):
+        w = synthgen.WORKLOADS[workload]
+        Bw = args.batch or w.B
+        S_l = w.S // P
+        qkv = [synthgen.gen_qkv_shard(0, t, (Bw, w.S, w.H, w.D), rank * S_l, (rank + 1) * S_l, device=dev)
+               for t in range(3)]
+        plan = spa.Plan(comm, Bw, w.S, w.H, w.D, stages=n_st)
+        return plan, qkv, torch.empty_like(qkv[0]), plan.workspace(dev)
+
+    def call(plan, qkv, out, ws):
+        if P == 1:
+            spa.spa_pipesp_attention_local(plan, [qkv[0]], [qkv[1]], [qkv[2]], [out], ws, stream)
+        else:
+            spa.spa_pipesp_attention(plan, *qkv, out, ws, stream)
+
+    def timed(plan, qkv, out, ws, n, warm, profile):
+        """Per-step CUDA-event times (ms) on the calling stream, L2 flushed (untimed) before every step."""
+        for _ in range(warm):
+            call(plan, qkv, out, ws)
         barrier()
-        for i in range(args.steps):
-            flush.zero_()                       # L2 flush between timed steps (untimed)
+        plan.set_option(spa.SPA_OPT_PROFILE, int(profile))
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        profs = []
+        for i in range(n):
+            flush.zero_()
             ev[i][0].record(stream)
-            step(*qkv, out)
+            call(plan, qkv, out, ws)
             ev[i][1].record(stream)
-            torch.cuda.synchronize()
-            prof = plan.last_profile()
-            attn_ms.append(sum(prof.attn_ms[k] for k in range(prof.n_stages)))
-            a2a_in.append(sum(prof.a2a_in_ms[k] for k in range(prof.n_stages)))
-            a2a_out.append(sum(prof.a2a_out_ms[k] for k in range(prof.n_stages)))
-            attn_launches += prof.attn_launches
-            copy_launches += prof.copy_launches
+            if profile:
+                torch.cuda.synchronize()
+                profs.append(plan.last_profile())
         barrier()
-    plan.set_option(spa.SPA_OPT_PROFILE, 0)
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    t_rank = sum(step_ms) / len(step_ms)
-    t = torch.tensor([t_rank], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_max = float(t.item())
+        plan.set_option(spa.SPA_OPT_PROFILE, 0)
+        return [a.elapsed_time(b) for a, b in ev], profs
+
+    def exposed_pct(plan, qkv, out, ws, t_layer, n):
+        """(t_layer - t_skipcomm) / t_layer: the same plan and schedule with the all-to-alls not issued."""
+        plan.set_option(spa.SPA_OPT_SKIP_COMM, 1)
+        ms, _ = timed(plan, qkv, out, ws, n, 2, False)
+        plan.set_option(spa.SPA_OPT_SKIP_COMM, 0)
+        t_nc = max_over_ranks(statistics.median(ms))
+        return max(0.0, (t_layer - t_nc) / t_layer * 100.0), t_nc
+
+    peaks, peak_src = load_peaks()
+    peak = peaks["bf16_tflops"]
+
+    # ---------------------------------------------------------------- headline
+    plan, qkv, out, ws = make(name, stages)
+    with ClockSampler(local) as clk:
+        step_ms, profs = timed(plan, qkv, out, ws, args.steps, args.warmup, True)
+    t_max = max_over_ranks(statistics.median(step_ms))
     flops = attn_flops(B, S, H, D)
     value = flops / (t_max * 1e-3) / 1e12
-
-    # exposed all-to-all: same plan and schedule with the transport skipped
-    exposed = None
+    attn_ms = [sum(p.attn_ms[k] for k in range(p.n_stages)) for p in profs]
+    a2a_in = [sum(p.a2a_in_ms[k] for k in range(p.n_stages)) for p in profs]
+    a2a_out = [sum(p.a2a_out_ms[k] for k in range(p.n_stages)) for p in profs]
+    launches = sum(p.attn_launches + p.copy_launches for p in profs)
+    exposed, t_nocomm = (None, None)
+    a2a = None
     if P > 1:
-        plan.set_option(spa.SPA_OPT_SKIP_COMM, 1)
-        for _ in range(2):
-            step(*qkv, out)
-        barrier()
-        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        for i in range(args.steps):
-            flush.zero_()
-            ev2[i][0].record(stream)
-            step(*qkv, out)
-            ev2[i][1].record(stream)
-        barrier()
-        plan.set_option(spa.SPA_OPT_SKIP_COMM, 0)
-        t2 = torch.tensor([sum(a.elapsed_time(b) for a, b in ev2) / args.steps], device=dev)
-        if world > 1:
-            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-        exposed = max(0.0, (t_max - float(t2.item())) / t_max * 100.0)
+        exposed, t_nocomm = exposed_pct(plan, qkv, out, ws, t_max, args.steps)
+        sent = _a2a_send_bytes(plan, rank)
+        a2a_ms = statistics.median([a + b for a, b in zip(a2a_in, a2a_out)])
+        a2a = {"in_ms": statistics.median(a2a_in), "out_ms": statistics.median(a2a_out),
+               "sent_bytes_per_rank": sent, "gbs_per_rank": sent / (a2a_ms * 1e-3) / 1e9 if a2a_ms > 0 else None,
+               "vs_nvlink_900": (sent / (a2a_ms * 1e-3) / 1e9) / NVLINK_GBS if a2a_ms > 0 else None}
+    roof_t = max(flops / P / (peak * 1e12), (_a2a_send_bytes(plan, rank) if P > 1 else 0) / (NVLINK_GBS * 1e9))
+    overlapped = {"t_roofline_ms": roof_t * 1e3, "frac": roof_t * 1e3 / t_max,
+                  "formula": "max(4BS^2HD/(P*peak_bf16), a2a bytes sent per rank / 900 GB/s)"}
 
     # end-to-end through the public API with host buffers: H2D inputs, the call, D2H output.  One GPU: the
     # library's host-buffer call (spa_attention_host), which overlaps head group i's attention with group i+1's
@@ -306,47 +340,44 @@ def run_ours(args):
         for _ in range(2):
             spa.spa_attention_host(hplan, *hq, hout, hws, stream)
         barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         for i in range(args.steps):
+            ev[i][0].record(stream)
             spa.spa_attention_host(hplan, *hq, hout, hws, stream)
-        e1.record(stream)
+            ev[i][1].record(stream)
         barrier()
-        te = float(e0.elapsed_time(e1)) / args.steps
+        te = statistics.median([a.elapsed_time(b) for a, b in ev])
         e2e = {"value": flops / (te * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": te,
                "h2d_bytes_per_step": sum(x.numel() * x.element_size() for x in hq),
                "d2h_bytes_per_step": hout.numel() * hout.element_size(),
                "path": f"spa_attention_host, {hplan.stage_split[0]} head groups pipelined H2D / attention / D2H"}
         hplan.close()
+        del hws
     elif not args.no_e2e:
         hq = [x.cpu().pin_memory() for x in qkv]
         hout = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
         dq = [torch.empty_like(x) for x in qkv]
         dout = torch.empty_like(out)
         barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         for i in range(args.steps):
+            ev[i][0].record(stream)
             for d_, h_ in zip(dq, hq):
                 d_.copy_(h_, non_blocking=True)
-            step(*dq, dout)
+            call(plan, dq, dout, ws)
             hout.copy_(dout, non_blocking=True)
-        e1.record(stream)
+            ev[i][1].record(stream)
         barrier()
-        te = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": flops / (float(te.item()) * 1e-3) / 1e12, "unit": "TFLOP/s",
-               "ms_per_step": float(te.item()),
+        te = max_over_ranks(statistics.median([a.elapsed_time(b) for a, b in ev]))
+        e2e = {"value": flops / (te * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": te,
                "h2d_bytes_per_step": sum(x.numel() * x.element_size() for x in hq),
-               "d2h_bytes_per_step": hout.numel() * hout.element_size()}
+               "d2h_bytes_per_step": hout.numel() * hout.element_size(),
+               "path": "per rank: H2D of the shard, spa_pipesp_attention, D2H (in sequence)"}
 
     # roofline of the dominant kernel (attention): algorithmic FLOPs per launch / measured duration
-    peaks, peak_src = load_peaks()
-    rank_attn_flops = attn_flops(B, S, H, D) / P
-    attn_ms_avg = sum(attn_ms) / len(attn_ms)
-    achieved = rank_attn_flops / (attn_ms_avg * 1e-3) / 1e12
-    peak = peaks["bf16_tflops"]
+    rank_attn_flops = flops / P
+    attn_ms_med = statistics.median(attn_ms)
+    achieved = rank_attn_flops / (attn_ms_med * 1e-3) / 1e12
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -357,7 +388,36 @@ def run_ours(args):
                 "traffic": traffic, "peak_source": f"{peak_src} bf16_tflops (burst cuBLAS 8192^3)",
                 "frac_of_sustained": achieved / peaks.get("bf16_tflops_sustained", peak),
                 "frac_of_datasheet_2250": achieved / 2250.0, "kernel": "attn_fwd_kernel (tcgen05)",
-                "attn_ms_per_step": attn_ms_avg}
+                "attn_ms_per_step": attn_ms_med,
+                "algorithmic": f"4*B*S^2*H*D/P = {rank_attn_flops:.4g} FLOP per rank per step"}
+    split = list(plan.stage_split)
+    plan.close()
+    del ws, qkv, out
+
+    # ---------------------------------------------------------------- north-star block (720p, N_st sweep)
+    north = None
+    if args.north_star == 1 or (args.north_star == -1 and P == 8):
+        wn = synthgen.WORKLOADS["hy720p129f"]
+        fl = attn_flops(wn.B, wn.S, wn.H, wn.D)
+        n = max(3, min(args.steps, 10))
+        sweep = []
+        for st in NORTH_STAR_STAGES:
+            pl, x, o, w_ = make("hy720p129f", st)
+            ms, pr = timed(pl, x, o, w_, n, 3, True)
+            t = max_over_ranks(statistics.median(ms))
+            ex, tnc = exposed_pct(pl, x, o, w_, t, n) if P > 1 else (0.0, t)
+            sent = _a2a_send_bytes(pl, rank) if P > 1 else 0
+            a2a_ms = statistics.median([sum(p.a2a_in_ms[k] + p.a2a_out_ms[k] for k in range(p.n_stages)) for p in pr])
+            troof = max(fl / P / (peak * 1e12), sent / (NVLINK_GBS * 1e9)) * 1e3
+            sweep.append({"stages": st, "stage_split": list(pl.stage_split), "ms_per_layer": t,
+                          "tflops": fl / (t * 1e-3) / 1e12, "exposed_a2a_pct": ex, "ms_skip_comm": tnc,
+                          "a2a_gbs_per_rank": max_over_ranks(sent / (a2a_ms * 1e-3) / 1e9) if a2a_ms > 0 else None,
+                          "frac_overlapped_roofline": troof / t, "t_roofline_ms": troof})
+            pl.close()
+            del x, o, w_
+        best = min(sweep, key=lambda r: r["ms_per_layer"])
+        north = {"workload": "hy720p129f", "P": P, "best": best, "sweep": sweep,
+                 "target": ">= 0.60 of the overlapped roofline, <= 10 % exposed all-to-all (BASELINE.json)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -371,18 +431,30 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": t_max, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded splitmix64 Irwin-Hall, D0, seed 0)",
             "config": {"workload": name, "B": B, "S": S, "H": H, "D": D, "P": P, "stages": stages,
-                       "stage_split": list(plan.stage_split), "parallelism": f"ulysses-sp{P}" if P > 1 else "single",
+                       "stage_split": split,
+                       "parallelism": f"ulysses-sp{P} (PipeSP)" if P > 1 else "single",
+                       "timing": "median of per-step CUDA events, max over ranks",
                        "l2": "flushed between timed steps (256 MiB memset, untimed); inputs > L2"},
-            "exposed_a2a_pct": exposed,
-            "a2a_ms_per_step": {"in": sum(a2a_in) / len(a2a_in), "out": sum(a2a_out) / len(a2a_out)} if P > 1 else None,
-            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": attn_launches + copy_launches,
-            "roofline": roofline, "cpu_baseline": cpu,
+            "exposed_a2a_pct": exposed, "ms_skip_comm": t_nocomm, "a2a": a2a, "overlapped_roofline": overlapped,
+            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches,
+            "roofline": roofline, "cpu_baseline": cpu, "north_star": north,
         }
         print(json.dumps(line), flush=True)
-    plan.close()
     comm.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def spawn(args) -> int:
+    """N > 1 without a launcher: re-run this script under torch.distributed.run, one rank per GPU."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    argv = [a for a in sys.argv[1:] if a != "--spawn"]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -391,6 +463,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif "WORLD_SIZE" not in os.environ and (args.gpus > 1 or args.spawn):
+        sys.exit(spawn(args))
     else:
         run_ours(args)
 

@@ -1,7 +1,23 @@
-"""Full-size parity at the BASELINE.json shapes, in the launch configuration bench.py times:
-sampled output rows against the fp64 oracle (each output row depends only on its own query row
-and the full K/V of its head, so a sampled row is an exact check), edge rows included
-(first/last token of every rank shard, the ragged tail of 720p), plus properties at full size."""
+"""Full-size parity at the BASELINE.json shapes, in the launch configurations bench.py times.
+
+Per (config, value distribution) one test: the inputs are generated at full size, every path that
+serves the config runs on them, and the outputs are compared with the fp64 oracle on >= 1024 sampled
+query rows x 6 heads spread over H (SURVEY.md §8(c) "Sampled rows at scale").  Each output row depends
+only on its own query row and the full K/V of its head (Alg. 1 l.3), so a sampled row is
+an exact check.  The sample holds uniform random rows plus every shard-edge row for P in {6, 7, 8}
+(including the uneven 7-way shards of Aco 7+1), the query-chunk edges of N_st = 24, and the 16 rows of
+the ragged last 128-row tile of 720p.
+
+Paths: the single-GPU kernel and the 1-rank plan call (the N=1 bench configuration), PipeSP over P = 8
+virtual ranks with N_st in {1, 3, 24} (+ the direct transport at N_st = 3), Aco 6+2 and the paper's 7+1
+ at 720p, Ring-Attention over 8 ranks at OSP, and a key-padding mask at HY-544p.  The
+bit-identity of every staged path with the single kernel (R18) is asserted on the whole tensor.
+
+Worst max-abs / rel-L2 per (config, distribution, path) are printed and, when SPA_PARITY_LOG names a
+file, appended to it as JSON lines (profiles/r02/parity_fullsize.jsonl)."""
+import json
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -11,97 +27,155 @@ import synthgen
 from paper_2511_12056_b200 import spa
 from tests import gpu_util as U
 
-pytestmark = [pytest.mark.gpu, pytest.mark.timeout(1200)]
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(1800)]
+
+HEADS = [0, 5, 9, 14, 18, 23]      # 6 heads spread over H = 24
+N_RANDOM = 1024
 
 
-def _gen(B, S, H, D, seed=0):
-    return [synthgen.gen_qkv_shard(seed, t, (B, S, H, D), 0, S, device="cuda") for t in range(3)]
+def _gen(w, dist, seed):
+    return [synthgen.gen_qkv_shard(seed, t, (w.B, w.S, w.H, w.D), 0, w.S, dist=dist, device="cuda")
+            for t in range(3)]
 
 
-def _check_rows(q, k, v, out, rows, heads, b=0):
-    """oracle on the sampled (row, head) pairs; returns (max_abs, rel_l2) over all of them."""
-    got, ref = [], []
-    for h in heads:
-        Q = q[b, rows, h].double().cpu().numpy()
-        K = k[b, :, h].double().cpu().numpy()
-        V = v[b, :, h].double().cpu().numpy()
-        ref.append(oracle.attention_rows(Q, K, V))
-        got.append(out[b, rows, h].double().cpu().numpy())
-    got, ref = np.stack(got), np.stack(ref)
-    d = got - ref
-    return float(np.abs(d).max()), float(np.linalg.norm(d) / np.linalg.norm(ref))
+def _bounds(S, P):
+    """Shard starts of P source ranks, lengths differing by <= 1 (R9)."""
+    lens = [S // P + (1 if r < S % P else 0) for r in range(P)]
+    return np.concatenate([[0], np.cumsum(lens)]).tolist()
 
 
-def _sample(S, P, n=48, seed=0):
+def sample_rows(S, seed=0):
     rng = np.random.default_rng(seed)
-    S_l = S // P
-    edges = [x for r in range(P) for x in (r * S_l, r * S_l + S_l - 1)]
-    tail = list(range((S // 128) * 128, S)) if S % 128 else []
-    rows = sorted(set(rng.integers(0, S, n).tolist() + edges + tail[:16]))
-    return torch.tensor(rows)
+    rows = set(rng.integers(0, S, N_RANDOM).tolist())
+    for P in (6, 7, 8):
+        b = _bounds(S, P)
+        for r in range(P):
+            rows.update((b[r], b[r + 1] - 1))
+            if P == 8:   # query-chunk edges of N_st = 24 at P = 8 (C = 8 chunks per head, DESIGN.md R7)
+                L = b[r + 1] - b[r]
+                rows.update(b[r] + c * L // 8 for c in range(8))
+                rows.update(b[r] + (c + 1) * L // 8 - 1 for c in range(8))
+    rows.update(range((S // 128) * 128, S))   # the ragged last tile (16 rows at 720p)
+    return torch.tensor(sorted(rows))
 
 
-def _pipesp(P, q, k, v, stages, direct=False):
+class Ref:
+    """fp64 oracle rows for the sampled (row, head) pairs of one input set."""
+
+    def __init__(self, q, k, v, rows, heads, kv_len=None):
+        self.rows, self.heads = rows, heads
+        ref = []
+        for h in heads:
+            L = q.shape[1] if kv_len is None else kv_len
+            Q = q[0, rows, h].double().cpu().numpy()
+            K = k[0, :L, h].double().cpu().numpy()
+            V = v[0, :L, h].double().cpu().numpy()
+            ref.append(oracle.attention_rows(Q, K, V))
+        self.ref = np.stack(ref)
+
+    def errors(self, out):
+        got = np.stack([out[0, self.rows, h].double().cpu().numpy() for h in self.heads])
+        d = got - self.ref
+        return (float(np.abs(d).max()), float(np.linalg.norm(d) / np.linalg.norm(self.ref)),
+                float(np.abs(self.ref).max()))
+
+
+def _log(config, dist, path, err, n_pairs):
+    ma, rl, refmax = err
+    rec = {"config": config, "dist": dist, "path": path, "max_abs": ma, "rel_l2": rl, "ref_max_abs": refmax,
+           "max_abs_over_ref_max": ma / refmax, "pairs": n_pairs, "tol": {"max_abs": U.MAX_ABS, "rel_l2": U.REL_L2}}
+    print(json.dumps(rec))
+    dst = os.environ.get("SPA_PARITY_LOG")
+    if dst:
+        with open(dst, "a") as f:
+            f.write(json.dumps(rec) + "\n")
+    assert ma <= U.MAX_ABS and rl <= U.REL_L2, rec
+
+
+def _same(a, b):
+    return torch.equal(a.view(torch.int16), b.view(torch.int16))
+
+
+def _shards(x, bounds):
+    return [x[:, bounds[r]:bounds[r + 1]].contiguous() for r in range(len(bounds) - 1)]
+
+
+def _sp(P, q, k, v, stages, n_src=0, direct=False, ring=False, kv_len=None):
     B, S, H, D = q.shape
-    plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=stages)
+    plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=stages, n_src=n_src, ring=ring)
     if direct:
         plan.set_option(spa.SPA_OPT_DIRECT, 1)
-    S_l = S // P
-    shards = [[x[:, r * S_l:(r + 1) * S_l].contiguous() for r in range(P)] for x in (q, k, v)]
-    outs = [torch.empty_like(t) for t in shards[0]]
+    if kv_len is not None:
+        plan.set_kv_len(kv_len)
+    b = _bounds(S, n_src or P)
+    qs, ks, vs = (_shards(x, b) for x in (q, k, v))
+    outs = [torch.empty_like(t) for t in qs]
     ws = plan.workspace()
-    spa.spa_pipesp_attention_local(plan, *shards, outs, ws)
+    call = spa.spa_ring_attention_local if ring else (
+        spa.spa_aco_attention_local if n_src else spa.spa_pipesp_attention_local)
+    call(plan, qs, ks, vs, outs, ws)
     torch.cuda.synchronize()
-    del ws
+    del ws, qs, ks, vs
+    plan.close()
     return torch.cat(outs, dim=1)
 
 
-@pytest.mark.parametrize("name", ["osp480p93f", "hy544p129f"])
-def test_single_gpu_baseline_configs(name):
-    """configs[1] / configs[2] at P=1 (the N=1 bench configuration: one plan call on all heads)."""
-    w = synthgen.WORKLOADS[name]
-    q, k, v = _gen(w.B, w.S, w.H, w.D)
-    out = torch.empty_like(q)
+CASES = [(c, d) for c in ("osp480p93f", "hy544p129f", "hy720p129f") for d in ("D0", "D1", "D4")]
+
+
+@pytest.mark.parametrize("config,dist", CASES)
+def test_fullsize_sampled_rows(config, dist):
+    w = synthgen.WORKLOADS[config]
+    seed = {"D0": 0, "D1": 1, "D4": 4}[dist]
+    q, k, v = _gen(w, dist, seed)
+    rows = sample_rows(w.S, seed)
+    assert len(rows) >= N_RANDOM
+    ref = Ref(q, k, v, rows, HEADS)
+    npairs = len(rows) * len(HEADS)
+
+    single = spa.attention(q, k, v)
+    torch.cuda.synchronize()
+    assert not torch.isnan(single.float()).any()
+    _log(config, dist, "single_kernel", ref.errors(single), npairs)
+
+    # the N=1 bench configuration: a 1-rank plan call on all heads
     plan = spa.Plan(spa.Comm.loopback(1), w.B, w.S, w.H, w.D)
-    spa.spa_pipesp_attention_local(plan, [q], [k], [v], [out], plan.workspace())
+    out1 = torch.empty_like(q)
+    spa.spa_pipesp_attention_local(plan, [q], [k], [v], [out1], plan.workspace())
     torch.cuda.synchronize()
-    assert not torch.isnan(out.float()).any()
-    ma, rl = _check_rows(q, k, v, out, _sample(w.S, 1), heads=[0, w.H // 2, w.H - 1])
-    assert ma <= U.MAX_ABS and rl <= U.REL_L2, (ma, rl)
+    assert _same(out1, single)
+    _log(config, dist, "plan_P1", ref.errors(out1), npairs)
+    del out1
 
-
-def test_720p_p8_pipesp_stages_bit_identical():
-    """configs[3]: 720p x 129f (S = 118,800, ragged tail of 16 rows), P = 8 virtual ranks, N_st in {1, 3, 24}:
-    sampled rows vs the oracle, and every stage split bit-identical to the single-GPU kernel."""
-    w = synthgen.WORKLOADS["hy720p129f"]
-    q, k, v = _gen(w.B, w.S, w.H, w.D)
-    single = spa.attention(q, k, v)
-    torch.cuda.synchronize()
-    ma, rl = _check_rows(q, k, v, single, _sample(w.S, 8, n=32), heads=[0, 23])
-    assert ma <= U.MAX_ABS and rl <= U.REL_L2, (ma, rl)
-    for st in (1, 3, 24):
-        out = _pipesp(8, q, k, v, st)
-        assert torch.equal(out.view(torch.int16), single.view(torch.int16)), st
+    for st in (1, 3, 24):   # PipeSP over 8 virtual ranks; N_st = 1 is Ulysses
+        out = _sp(8, q, k, v, st)
+        assert _same(out, single), st
+        _log(config, dist, f"pipesp_P8_Nst{st}", ref.errors(out), npairs)
         del out
-    out = _pipesp(8, q, k, v, 3, direct=True)   # SPA_OPT_DIRECT: the f1 data path (loopback model)
-    assert torch.equal(out.view(torch.int16), single.view(torch.int16))
+    out = _sp(8, q, k, v, 3, direct=True)     # SPA_OPT_DIRECT data path (loopback model)
+    assert _same(out, single)
+    del out
 
-
-def test_aco_720p_6_plus_2():
-    """configs[4]: Aco, shards on 6 denoising ranks, heads over 6+2 owners, S = 118,800."""
-    w = synthgen.WORKLOADS["hy720p129f"]
-    q, k, v = _gen(w.B, w.S, w.H, w.D, seed=1)
-    single = spa.attention(q, k, v)
-    plan = spa.Plan(spa.Comm.loopback(8), w.B, w.S, w.H, w.D, stages=3, n_src=6)
-    S_l = w.S // 6
-    shards = [[x[:, r * S_l:(r + 1) * S_l].contiguous() for r in range(6)] for x in (q, k, v)]
-    outs = [torch.empty_like(t) for t in shards[0]]
-    spa.spa_aco_attention_local(plan, *shards, outs, plan.workspace())
-    torch.cuda.synchronize()
-    out = torch.cat(outs, dim=1)
-    assert torch.equal(out.view(torch.int16), single.view(torch.int16))
-    ma, rl = _check_rows(q, k, v, out, _sample(w.S, 6, n=24, seed=3), heads=[5])
-    assert ma <= U.MAX_ABS and rl <= U.REL_L2, (ma, rl)
+    if config == "hy720p129f":                 # Aco: configs[4] 6+2, and the paper's 7+1 (uneven shards)
+        for n_src in (6, 7):
+            out = _sp(8, q, k, v, 3, n_src=n_src)
+            assert _same(out, single), n_src
+            _log(config, dist, f"aco_{n_src}+{8 - n_src}", ref.errors(out), npairs)
+            del out
+    if config == "osp480p93f":                 # Ring-Attention over 8 ranks (R21): a different summation order
+        out = _sp(8, q, k, v, 1, ring=True)
+        _log(config, dist, "ring_P8", ref.errors(out), npairs)
+        del out
+    if config == "hy544p129f":                 # key-padding mask (R20): 70,001 of 76,032 keys valid
+        L = 70_001
+        kv_len = torch.tensor([L], dtype=torch.int32, device="cuda")
+        masked = spa.attention(q, k, v, kv_len=kv_len)
+        torch.cuda.synchronize()
+        mref = Ref(q, k, v, rows, HEADS, kv_len=L)
+        _log(config, dist, "masked_single", mref.errors(masked), npairs)
+        out = _sp(4, q, k, v, 2, kv_len=kv_len)
+        assert _same(out, masked)
+        _log(config, dist, "masked_pipesp_P4_Nst2", mref.errors(out), npairs)
 
 
 def test_fullsize_closed_forms():
@@ -114,69 +188,3 @@ def test_fullsize_closed_forms():
     out = spa.attention(q, k, v).double()
     mean = v.double().mean(dim=1, keepdim=True)
     assert (out - mean).abs().max().item() < 1e-3
-
-
-def test_ring_osp_p8_fullsize():
-    """Ring-Attention (R21) at configs[1] size over 8 virtual ranks: sampled rows vs the oracle."""
-    w = synthgen.WORKLOADS["osp480p93f"]
-    q, k, v = _gen(w.B, w.S, w.H, w.D, seed=2)
-    P = 8
-    plan = spa.Plan(spa.Comm.loopback(P), w.B, w.S, w.H, w.D, ring=True)
-    S_l = w.S // P
-    shards = [[x[:, r * S_l:(r + 1) * S_l].contiguous() for r in range(P)] for x in (q, k, v)]
-    outs = [torch.empty_like(t) for t in shards[0]]
-    ws = plan.workspace()
-    spa.spa_ring_attention_local(plan, *shards, outs, ws)
-    torch.cuda.synchronize()
-    del ws
-    out = torch.cat(outs, dim=1)
-    ma, rl = _check_rows(q, k, v, out, _sample(w.S, P, n=32, seed=4), heads=[0, 23])
-    assert ma <= U.MAX_ABS and rl <= U.REL_L2, (ma, rl)
-
-
-def test_key_padding_mask_fullsize():
-    """Key-padding mask (R20) at configs[2] size: kv_len = 70,001 of 76,032 keys, sampled rows vs the oracle on
-    the truncated keys, and the masked PipeSP at P = 4 bit-identical to the masked single-GPU kernel."""
-    w = synthgen.WORKLOADS["hy544p129f"]
-    q, k, v = _gen(w.B, w.S, w.H, w.D, seed=3)
-    L = 70_001
-    kv_len = torch.tensor([L], dtype=torch.int32, device="cuda")
-    single = spa.attention(q, k, v, kv_len=kv_len)
-    torch.cuda.synchronize()
-    ma, rl = _check_rows(q, k[:, :L], v[:, :L], single, _sample(w.S, 4, n=24, seed=5), heads=[7])
-    assert ma <= U.MAX_ABS and rl <= U.REL_L2, (ma, rl)
-    P = 4
-    plan = spa.Plan(spa.Comm.loopback(P), w.B, w.S, w.H, w.D, stages=2)
-    plan.set_kv_len(kv_len)
-    S_l = w.S // P
-    shards = [[x[:, r * S_l:(r + 1) * S_l].contiguous() for r in range(P)] for x in (q, k, v)]
-    outs = [torch.empty_like(t) for t in shards[0]]
-    ws = plan.workspace()
-    spa.spa_pipesp_attention_local(plan, *shards, outs, ws)
-    torch.cuda.synchronize()
-    del ws
-    assert torch.equal(torch.cat(outs, dim=1).view(torch.int16), single.view(torch.int16))
-
-
-def test_aco_720p_seven_plus_one():
-    """The paper's Aco example at configs[3] size: S = 118,800 over 7 denoising ranks (uneven:
-    16,972 / 16,971 tokens), 24 heads over 7 + 1 owners; bit-identical to the single-GPU kernel."""
-    w = synthgen.WORKLOADS["hy720p129f"]
-    q, k, v = _gen(w.B, w.S, w.H, w.D, seed=4)
-    single = spa.attention(q, k, v)
-    plan = spa.Plan(spa.Comm.loopback(8), w.B, w.S, w.H, w.D, stages=3, n_src=7)
-    shards, t = [[], [], []], 0
-    for r in range(7):
-        ln = w.S // 7 + (1 if r < w.S % 7 else 0)
-        for i, x in enumerate((q, k, v)):
-            shards[i].append(x[:, t:t + ln].contiguous())
-        t += ln
-    outs = [torch.empty_like(x) for x in shards[0]]
-    ws = plan.workspace()
-    spa.spa_aco_attention_local(plan, *shards, outs, ws)
-    torch.cuda.synchronize()
-    del ws
-    out = torch.cat(outs, dim=1)
-    assert torch.equal(out.view(torch.int16), single.view(torch.int16))
-    ma, rl = _check_rows(q, k, v, out, _sample(w.S, 7, n=16, seed=6), heads=[21])
-    assert ma <= U.MAX_ABS and rl <= U.REL_L2, (ma, rl)
