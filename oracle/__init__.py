@@ -13,13 +13,15 @@ Contents
                 per-stage output all-to-all of Alg. 1, the
                 Psi / Psi_g layout fix, Aco's relay
                 (PAPER.md:163-169), head padding.
+  projection.py the QKV linear projections X W^T + b rounded once
+                to bf16, and the SP layer from hidden states.
 
 Parity status: every function here is pinned by ``tests/test_oracle_*.py`` against
 values that do not come from the oracle itself (paper worked values, closed forms,
 brute force, library routines); see DESIGN.md §Oracle pins.  No function is
 "parity unpinned".
 """
-from . import attention, sp  # noqa: F401
+from . import attention, projection, sp  # noqa: F401
 from .attention import (attention_rows, softmax_weights, mha_unsharded, build_library,  # noqa: F401
                         key_valid_from_lengths, attention_rows_lse,
                         library_path)

@@ -38,10 +38,12 @@ __all__ = [
     "splitmix64", "uniform24", "irwin_hall4", "bf16_bits_from_f64",
     "gen_elements", "gen_qkv_shard", "gen_head_rows", "bf16_bits_to_f64",
     "Workload", "WORKLOADS", "tokens_for_video",
+    "TENSOR_X", "TENSOR_W", "TENSOR_BIAS", "gen_hidden_shard", "gen_qkv_weight", "gen_qkv_bias",
 ]
 
 TENSOR_Q, TENSOR_K, TENSOR_V = 0, 1, 2
 _NOISE_K = 3  # D4 noise stream
+TENSOR_X, TENSOR_W, TENSOR_BIAS = 4, 5, 6   # hidden states, fused QKV weight, its bias (QKV projection, f3)
 
 _M64 = (1 << 64)
 
@@ -186,3 +188,35 @@ WORKLOADS = {
     "hy544p129f": Workload("hy544p129f", 1, 76_032, 24, 128),
     "hy720p129f": Workload("hy720p129f", 1, 118_800, 24, 128),
 }
+
+
+# ------------------------------------------------------------------ hidden states / QKV weights
+def _gen_flat(seed: int, tensor_id: int, n: int, sigma: float, device, start: int = 0,
+              chunk: int = 1 << 26) -> torch.Tensor:
+    """bf16 bits of sigma*IH4 for flat indices [start, start+n) of tensor `tensor_id` (int16 [n])."""
+    out = torch.empty(n, dtype=torch.int16, device=device)
+    for i in range(0, n, chunk):
+        j = min(n, i + chunk)
+        flat = torch.arange(start + i, start + j, device=device, dtype=torch.int64)
+        out[i:j] = bf16_bits_from_f64(sigma * irwin_hall4(seed, tensor_id, flat))
+    return out
+
+
+def gen_hidden_shard(seed: int, shape_global: Sequence[int], tok0: int, tok1: int, device="cpu") -> torch.Tensor:
+    """Rows [tok0, tok1) of the global hidden states X [B, S, C] (sigma = 1: LayerNorm-ed DiT activations)."""
+    B, S, C = shape_global
+    n = tok1 - tok0
+    out = torch.empty((B, n, C), dtype=torch.int16, device=device)
+    for b in range(B):
+        out[b].view(-1).copy_(_gen_flat(seed, TENSOR_X, n * C, 1.0, device, start=(b * S + tok0) * C))
+    return out.view(torch.bfloat16)
+
+
+def gen_qkv_weight(seed: int, C: int, H: int, D: int, device="cpu") -> torch.Tensor:
+    """Fused nn.Linear weight W [3*H*D, C] bf16, sigma = 1/sqrt(C) (variance-preserving init: Q, K, V ~ N(0, 1))."""
+    return _gen_flat(seed, TENSOR_W, 3 * H * D * C, 1.0 / math.sqrt(C), device).view(3 * H * D, C).view(torch.bfloat16)
+
+
+def gen_qkv_bias(seed: int, H: int, D: int, device="cpu") -> torch.Tensor:
+    """Bias [3*H*D] as fp32 values of bf16 numbers, sigma = 0.1."""
+    return _gen_flat(seed, TENSOR_BIAS, 3 * H * D, 0.1, device).view(torch.bfloat16).float()
