@@ -133,7 +133,9 @@ spa_status spa_plan_destroy(spa_plan *plan);
  *                          owners' receive regions and the attention epilogue stores each output row straight
  *                          into its source rank's output (no staging, exchange copies or unpack).  Loopback
  *                          plans only for now (the NVLink version needs registered NCCL windows); same bits. */
-enum { SPA_OPT_PROFILE = 1, SPA_OPT_SKIP_COMM = 2, SPA_OPT_COPROC_BUSY = 3, SPA_OPT_DIRECT = 4 };
+/*   SPA_OPT_COMM_SMS  n -> the persistent QKV-projection GEMM (spa_pipesp_qkv_attention*) leaves n SMs free so that
+ *                          the communication kernels of the overlapped all-to-alls get SMs at once (0..64; default 0) */
+enum { SPA_OPT_PROFILE = 1, SPA_OPT_SKIP_COMM = 2, SPA_OPT_COPROC_BUSY = 3, SPA_OPT_DIRECT = 4, SPA_OPT_COMM_SMS = 5 };
 spa_status spa_plan_set_option(spa_plan *plan, int option, int value);
 
 /* Key-padding mask for the following SP calls of this plan (Alg. 1's attention_mask, PAPER.md:85 and :90,
@@ -153,6 +155,7 @@ typedef struct {
     float pack_ms, unpack_ms;
     float attn_ms[64], a2a_in_ms[64], a2a_out_ms[64];
     int attn_launches, copy_launches; /* library kernels launched by the call */
+    int gemm_launches;                /* QKV-projection GEMMs (pack_ms is then the projection time) */
 } spa_profile;
 spa_status spa_plan_last_profile(spa_plan *plan, spa_profile *out);
 
@@ -187,6 +190,38 @@ spa_status spa_aco_attention_local(spa_plan *plan, const void *const q[], const 
 spa_status spa_plan_host_workspace_bytes(const spa_plan *plan, size_t *bytes);
 spa_status spa_attention_host(spa_plan *plan, const void *q, const void *k, const void *v, void *o, void *ws,
                               void *stream);
+
+/* ------------------------------------------------------------------ QKV projection fused with PipeSP
+ * The SP layer from the hidden states ("after each GPU computes its portion of the sub-sequence's
+ * Q, K, and V, three rounds of All-to-All ..."; the projections Q = X W_Q, K = X W_K, V = X W_V of PAPER.md:155-157,
+ * overlapped with the input all-to-alls as in PAPER.md:439).  Per head group kh of the plan's stage split, one
+ * tcgen05 GEMM computes this rank's X [B, S_r, C] times the head group's weight rows for EVERY destination rank and
+ * stores the result (fp32 accumulate + fp32 bias, bf16 RNE) straight into the stage's all-to-all send layout (the
+ * pack step is fused away); head group kh's input all-to-all then overlaps head group kh+1's GEMM, and the rest is
+ * spa_pipesp_attention.  Plans: Ulysses / PipeSP (n_src = 0, no head padding, no ring); SPA_OPT_DIRECT does not
+ * apply (staged transport).  Result = spa_pipesp_attention on bf16(X W^T + b), bit for bit.
+ *
+ *   w      bf16 [3*H*D, C], the fused nn.Linear weight: output feature o = t*H*D + k*D + d (t = 0 Q, 1 K, 2 V;
+ *          head k; dim d).  bias: fp32 [3*H*D] or NULL.  C: hidden dim, a positive multiple of 8.
+ *   w_packed  device buffer of spa_plan_qkv_weight_bytes(plan, C) bytes, written by spa_plan_pack_qkv_weight
+ *          (once per plan and weight; it depends on the plan's P and stage split): the weight rows of each head group
+ *          in [t][dest q][g*D] order followed by the bias in the same order as fp32.
+ *   x      bf16 [B, S_r, C] contiguous (this rank's sequence shard of the hidden states; loopback: one per rank).
+ *   ws     spa_plan_qkv_workspace_bytes(): spa_plan_workspace_bytes() when nranks > 1; the projected Q, K, V
+ *          [B, S, H, D] when nranks == 1. */
+spa_status spa_plan_qkv_weight_bytes(const spa_plan *plan, int C, size_t *bytes);
+spa_status spa_plan_qkv_workspace_bytes(const spa_plan *plan, size_t *bytes);
+spa_status spa_plan_pack_qkv_weight(spa_plan *plan, int C, const void *w, const float *bias, void *w_packed,
+                                    void *stream);
+spa_status spa_pipesp_qkv_attention(spa_plan *plan, int C, const void *x, const void *w_packed, void *out, void *ws,
+                                    void *stream);
+spa_status spa_pipesp_qkv_attention_local(spa_plan *plan, int C, const void *const x[], const void *w_packed,
+                                          void *const out[], void *ws, void *stream);
+/* The projections alone, in the standard layout: q, k, v = bf16 [B, S_r, H, D] of source rank `rank` (its x is
+ * [B, S_r, C]; NCCL plans: rank must be the comm's own).  Same GEMM and rounding as the fused calls, so
+ * spa_pipesp_attention on these q, k, v equals spa_pipesp_qkv_attention bit for bit. */
+spa_status spa_qkv_projection(spa_plan *plan, int C, int rank, const void *x, const void *w_packed, void *q, void *k,
+                              void *v, void *stream);
 
 /* Ring attention (shape.ring = 1; R21): q, k, v, out as above ([B, S/P, H, D], any H).  Rank r
  * attends to the K/V shard of rank (r - t) mod P at step t; the shards travel the ring r-1 -> r -> r+1 on

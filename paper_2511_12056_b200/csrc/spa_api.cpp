@@ -111,6 +111,7 @@ struct spa_plan {
     long long ws_rank_bytes = 0;
     // options
     bool profile = false, skip_comm = false, coproc_busy = false, direct = false;
+    int comm_sms = 0;   // SMs the persistent QKV GEMM leaves free for communication kernels (SPA_OPT_COMM_SMS)
     // runtime resources (lazy)
     std::vector<cudaEvent_t> sync_ev;  // scheduling events (no timing)
     std::vector<cudaEvent_t> prof_ev;  // timing events
@@ -118,7 +119,7 @@ struct spa_plan {
     bool have_profile = false;
     int prof_stages = 0;   // stages the last profiled call executed (spa_profile.n_stages)
     std::map<std::string, int> prof_idx;
-    int attn_launches = 0, copy_launches = 0;
+    int attn_launches = 0, copy_launches = 0, gemm_launches = 0;
     cudaStream_t sc_alt = nullptr;  // second compute stream: odd stages, so stage k+1 fills stage k's wave tail
 };
 
@@ -338,7 +339,44 @@ struct Exec {  // everything one call needs
     int in_tensors = 7;
     int q_recv_buf = BUF_WS, o_send_buf = BUF_WS;
     bool has_pack = true;
+    // QKV projection fused with the pack: xin = hidden states [B, S_r, C] per local source rank
+    bool qkv = false;
+    std::vector<const void *> xin;
+    const uint8_t *wp = nullptr;   // packed weight + bias (spa_plan_pack_qkv_weight)
+    int C = 0;
 };
+
+// ------------------------------------------------------------------ packed QKV weight
+// [G_h][t < 3][q < P][r < g*D][C] bf16 = W[t*H*D + (q*h + kh*g)*D + r][C], then the bias in the same column order
+// as fp32 [G_h][3][P][g*D] at a 256-byte aligned offset.  Head group kh's GEMM reads a contiguous [3*P*g*D][C].
+long long qkv_cols(const spa_plan *p) { return 3LL * p->P * p->split.g * p->sh.D; }
+long long qkv_bias_off(const spa_plan *p, int C) { return align_up((long long)p->split.G_h * qkv_cols(p) * C * 2, 256); }
+long long qkv_packed_bytes(const spa_plan *p, int C) {
+    return qkv_bias_off(p, C) + (long long)p->split.G_h * qkv_cols(p) * 4;
+}
+
+// GEMM of head group kh for the hidden states x of source rank r (M = B * len[r] tokens) into dst[t] + q*q_stride +
+// m*row_stride + r (elements; see QkvProblem).
+spa_status launch_qkv(spa_plan *p, const void *x, const uint8_t *wp, int C, int r, int kh, void *const dst[3],
+                      long long q_stride, long long row_stride, cudaStream_t st) {
+    QkvProblem g{};
+    g.x = x;
+    g.w = wp + (long long)kh * qkv_cols(p) * C * 2;
+    g.bias = reinterpret_cast<const float *>(wp + qkv_bias_off(p, C)) + (long long)kh * qkv_cols(p);
+    g.M = p->sh.B * p->len[r];
+    g.N = (int)qkv_cols(p);
+    g.K = C;
+    for (int t = 0; t < 3; ++t) g.dst[t] = dst[t];
+    g.q_stride = q_stride;
+    g.row_stride = row_stride;
+    g.cols_per_q = p->split.g * p->sh.D;
+    g.cols_per_t = p->P * g.cols_per_q;
+    g.reserve_sms = p->comm_sms;
+    cudaError_t e = launch_qkv_gemm(g, st);
+    if (e != cudaSuccess) return fail(SPA_ERR_CUDA, std::string("qkv gemm: ") + cudaGetErrorString(e));
+    ++p->gemm_launches;
+    return SPA_OK;
+}
 
 uint8_t *resolve(const Exec &x, int rank, int buf, long long off) {
     const spa_plan *p = x.p;
@@ -421,6 +459,26 @@ spa_status run_attention(Exec &x, int k, cudaStream_t st) {
         a.kv_batch_stride = (long long)p->sh.S * s.g * p->sh.D;
         SPA_CHECK_CUDA(launch_attention(a, st));
         ++p->attn_launches;
+    }
+    return SPA_OK;
+}
+
+// QKV projections of every head group straight into the send layout (pack fused), one GEMM per (kh, local source);
+// ev_gemm[kh] marks head group kh's send regions complete.
+spa_status run_qkv_pack(Exec &x, cudaEvent_t *ev_gemm) {
+    spa_plan *p = x.p;
+    const Split &s = *x.s;
+    const int nr = (p->comm->kind == KIND_LOOPBACK) ? p->Psrc : (is_source(p, p->comm->rank) ? 1 : 0);
+    for (int kh = 0; kh < s.G_h; ++kh) {
+        for (int i = 0; i < nr; ++i) {
+            const int r = (p->comm->kind == KIND_LOOPBACK) ? i : p->comm->rank;
+            uint8_t *ws = resolve(x, r, BUF_WS, 0);
+            const long long base = idx_send(p, s, r, kh, 0, 0, 0) * 2;
+            void *dst[3] = {ws + p->off_sendQ + base, ws + p->off_sendK + base, ws + p->off_sendV + base};
+            SPA_TRY(launch_qkv(p, x.xin[i], x.wp, x.C, r, kh, dst, (long long)p->sh.B * p->len[r] * s.g * p->sh.D,
+                               (long long)s.g * p->sh.D, x.sc));
+        }
+        SPA_CHECK_CUDA(cudaEventRecord(ev_gemm[kh], x.sc));
     }
     return SPA_OK;
 }
@@ -577,10 +635,11 @@ spa_status execute(Exec &x) {
     spa_plan *p = x.p;
     p->attn_launches = 0;
     p->copy_launches = 0;
+    p->gemm_launches = 0;
     const Split &s = *x.s;
     const int N = s.n();
-    SPA_TRY(ensure_events(p, 4 + 3 * (size_t)N, p->profile ? 8 + 6 * (size_t)N : 0));
-    if (p->direct && p->P > 1 && x.has_attn && x.has_pack && x.has_out) return execute_direct(x);
+    SPA_TRY(ensure_events(p, 4 + 3 * (size_t)N + s.G_h, p->profile ? 8 + 6 * (size_t)N : 0));
+    if (p->direct && p->P > 1 && x.has_attn && x.has_pack && x.has_out && !x.qkv) return execute_direct(x);
     Prof pr{p};
     if (p->P == 1) {
         // one rank owns everything: attention straight on the caller's [B,S,H,D] buffers
@@ -588,6 +647,19 @@ spa_status execute(Exec &x) {
         if (x.has_attn) {
             AttnProblem a{};
             a.q = x.ptr.q[0]; a.k = x.ptr.k[0]; a.v = x.ptr.v[0]; a.o = x.ptr.out[0];
+            if (x.qkv) {   // projections into the workspace's [B, S, H, D] Q, K, V (spa_plan_qkv_workspace_bytes)
+                const long long E = (long long)p->sh.B * p->sh.S * p->sh.H * p->sh.D * 2;
+                void *dst[3] = {x.ptr.ws, x.ptr.ws + E, x.ptr.ws + 2 * E};
+                pr.begin("pack", x.sc);
+                for (int kh = 0; kh < s.G_h; ++kh) {
+                    void *d[3] = {(uint8_t *)dst[0] + (long long)kh * s.g * p->sh.D * 2,
+                                  (uint8_t *)dst[1] + (long long)kh * s.g * p->sh.D * 2,
+                                  (uint8_t *)dst[2] + (long long)kh * s.g * p->sh.D * 2};
+                    SPA_TRY(launch_qkv(p, x.xin[0], x.wp, x.C, 0, kh, d, 0, (long long)p->sh.H * p->sh.D, x.sc));
+                }
+                pr.end("pack", x.sc);
+                a.q = dst[0]; a.k = dst[1]; a.v = dst[2];
+            }
             a.B = p->sh.B; a.Sq = a.Skv = p->sh.S; a.n_heads = p->sh.H; a.D = p->sh.D;
             a.kv_len = p->kv_len;
             a.q_tok_stride = a.kv_tok_stride = a.o_tok_stride = (long long)p->sh.H * p->sh.D;
@@ -612,20 +684,23 @@ spa_status execute(Exec &x) {
     x.sc_alt = p->sc_alt;
     cudaEvent_t *ev = p->sync_ev.data();
     cudaEvent_t ev_entry = ev[0], ev_pack = ev[1], ev_done = ev[2];
-    cudaEvent_t *ev_in = ev + 4, *ev_attn = ev + 4 + N, *ev_out = ev + 4 + 2 * N;
+    cudaEvent_t *ev_in = ev + 4, *ev_attn = ev + 4 + N, *ev_out = ev + 4 + 2 * N, *ev_gemm = ev + 4 + 3 * N;
 
     pr.begin("total", x.sc);
     SPA_CHECK_CUDA(cudaEventRecord(ev_entry, x.sc));
     SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_entry, 0));
     if (x.has_pack) {
         pr.begin("pack", x.sc);
-        SPA_TRY(run_pack(x));
+        if (x.qkv) SPA_TRY(run_qkv_pack(x, ev_gemm));
+        else SPA_TRY(run_pack(x));
         pr.end("pack", x.sc);
     }
     SPA_CHECK_CUDA(cudaEventRecord(ev_pack, x.sc));
-    SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_pack, 0));
+    // the staged pack is one launch; the fused projections complete head group by head group (ev_gemm)
+    if (!x.qkv) SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_pack, 0));
 
     auto issue_in = [&](int k) -> spa_status {
+        if (x.qkv && k % s.C == 0) SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_gemm[k / s.C], 0));
         const std::string nm = "in" + std::to_string(k);
         pr.begin(nm, x.sm);
         SPA_TRY(run_exchange(x, k, 0));
@@ -1048,6 +1123,10 @@ spa_status spa_plan_set_option(spa_plan *plan, int option, int value) {
         case SPA_OPT_PROFILE: plan->profile = value != 0; break;
         case SPA_OPT_SKIP_COMM: plan->skip_comm = value != 0; break;
         case SPA_OPT_COPROC_BUSY: plan->coproc_busy = value != 0; break;
+        case SPA_OPT_COMM_SMS:
+            if (value < 0 || value > 64) return fail(SPA_ERR_INVALID, "comm SMs must be in [0, 64]");
+            plan->comm_sms = value;
+            break;
         case SPA_OPT_DIRECT:
             if (value && plan->comm->kind == KIND_NCCL)
                 return fail(SPA_ERR_UNSUPPORTED, "direct transport: NVLink windows not built yet (loopback only)");
@@ -1090,6 +1169,7 @@ spa_status spa_plan_last_profile(spa_plan *plan, spa_profile *out) {
     }
     r.attn_launches = plan->attn_launches;
     r.copy_launches = plan->copy_launches;
+    r.gemm_launches = plan->gemm_launches;
     if (plan->U > 1 && plan->ring_plan->have_profile) {   // USP: the ring sub-plan's (last) call is the attention
         spa_profile rp{};
         SPA_TRY(spa_plan_last_profile(plan->ring_plan, &rp));
@@ -1144,6 +1224,120 @@ spa_status spa_aco_attention_local(spa_plan *plan, const void *const q[], const 
     if (!plan || !q || !k || !v || !out) return fail(SPA_ERR_INVALID, "NULL argument");
     if (plan->Psrc != plan->P && plan->coproc_busy) return fail(SPA_ERR_BUSY, "co-processor group busy");
     return attention_call(plan, n_local_srcs(plan), q, k, v, out, ws, stream, true, false);
+}
+
+// ------------------------------------------------------------------ QKV projection fused with PipeSP
+static spa_status qkv_check(const spa_plan *p, int C) {
+    if (!p) return fail(SPA_ERR_INVALID, "plan is NULL");
+    if (p->ring) return fail(SPA_ERR_UNSUPPORTED, "QKV projection calls need a Ulysses / PipeSP plan");
+    if (p->Psrc != p->P || p->Hp != p->sh.H)
+        return fail(SPA_ERR_UNSUPPORTED, "QKV projection calls: no co-processor ranks, no head padding");
+    if (C < 8 || C % 8) return fail(SPA_ERR_SHAPE, "hidden dim C must be a positive multiple of 8");
+    return SPA_OK;
+}
+
+spa_status spa_plan_qkv_weight_bytes(const spa_plan *plan, int C, size_t *bytes) {
+    SPA_TRY(qkv_check(plan, C));
+    if (!bytes) return fail(SPA_ERR_INVALID, "NULL argument");
+    *bytes = (size_t)qkv_packed_bytes(plan, C);
+    return SPA_OK;
+}
+
+spa_status spa_plan_qkv_workspace_bytes(const spa_plan *plan, size_t *bytes) {
+    if (!plan || !bytes) return fail(SPA_ERR_INVALID, "NULL argument");
+    SPA_TRY(qkv_check(plan, 8));
+    if (plan->P == 1) *bytes = (size_t)3 * plan->sh.B * plan->sh.S * plan->sh.H * plan->sh.D * 2;
+    else return spa_plan_workspace_bytes(plan, bytes);
+    return SPA_OK;
+}
+
+spa_status spa_plan_pack_qkv_weight(spa_plan *plan, int C, const void *w, const float *bias, void *w_packed,
+                                    void *stream) {
+    SPA_TRY(qkv_check(plan, C));
+    SPA_TRY(check_ptr(w, "w"));
+    SPA_TRY(check_ptr(w_packed, "w_packed"));
+    if (bias && reinterpret_cast<uintptr_t>(bias) % 16) return fail(SPA_ERR_INVALID, "bias not 16-byte aligned");
+    if (plan->comm->kind != KIND_HOST) SPA_CHECK_CUDA(cudaSetDevice(plan->comm->device));
+    else return fail(SPA_ERR_UNSUPPORTED, "host-only comm cannot execute");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const Split &s = plan->split;
+    const long long gD = (long long)s.g * plan->sh.D, H = plan->sh.H, D = plan->sh.D, h = plan->h, P = plan->P;
+    uint8_t *wp = reinterpret_cast<uint8_t *>(w_packed);
+    // weight rows: [kh][t][q] runs of g*D rows of W (row t*H*D + (q*h + kh*g)*D)
+    std::vector<CopyJob> jobs(1);
+    CopyJob &j = jobs[0];
+    j.src = reinterpret_cast<const uint8_t *>(w);
+    j.dst = wp;
+    j.count[0] = s.G_h; j.count[1] = 3; j.count[2] = P; j.count[3] = 1;
+    j.src_stride[0] = gD * C * 2; j.src_stride[1] = H * D * C * 2; j.src_stride[2] = h * D * C * 2;
+    j.dst_stride[0] = 3 * P * gD * C * 2; j.dst_stride[1] = P * gD * C * 2; j.dst_stride[2] = gD * C * 2;
+    j.run_bytes = gD * C * 2;
+    int launches = 0;
+    if (bias) {   // the same column permutation on the fp32 bias
+        CopyJob b = j;
+        b.src = reinterpret_cast<const uint8_t *>(bias);
+        b.dst = wp + qkv_bias_off(plan, C);
+        b.src_stride[0] = gD * 4; b.src_stride[1] = H * D * 4; b.src_stride[2] = h * D * 4;
+        b.dst_stride[0] = 3 * P * gD * 4; b.dst_stride[1] = P * gD * 4; b.dst_stride[2] = gD * 4;
+        b.run_bytes = gD * 4;
+        jobs.push_back(b);
+    } else {
+        SPA_CHECK_CUDA(cudaMemsetAsync(wp + qkv_bias_off(plan, C), 0, (size_t)s.G_h * qkv_cols(plan) * 4, st));
+    }
+    SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), st, &launches));
+    return SPA_OK;
+}
+
+static spa_status qkv_call(spa_plan *p, int C, int n, const void *const x[], const void *w_packed, void *const out[],
+                           void *ws, void *stream, bool local) {
+    SPA_TRY(qkv_check(p, C));
+    SPA_TRY(check_ptr(w_packed, "w_packed"));
+    Exec e{};
+    SPA_TRY(prepare(p, e, ws, stream, local));
+    if (p->P == 1) SPA_TRY(check_ptr(ws, "ws"));
+    e.s = &p->split;
+    e.qkv = true;
+    e.wp = reinterpret_cast<const uint8_t *>(w_packed);
+    e.C = C;
+    for (int i = 0; i < n; ++i) {
+        SPA_TRY(check_ptr(x[i], "x"));
+        SPA_TRY(check_ptr(out[i], "out"));
+        e.xin.push_back(x[i]);
+        e.ptr.q.push_back(nullptr); e.ptr.k.push_back(nullptr); e.ptr.v.push_back(nullptr);
+        e.ptr.out.push_back(out[i]);
+    }
+    return execute(e);
+}
+
+spa_status spa_pipesp_qkv_attention(spa_plan *plan, int C, const void *x, const void *w_packed, void *out, void *ws,
+                                    void *stream) {
+    return qkv_call(plan, C, 1, &x, w_packed, &out, ws, stream, false);
+}
+
+spa_status spa_pipesp_qkv_attention_local(spa_plan *plan, int C, const void *const x[], const void *w_packed,
+                                          void *const out[], void *ws, void *stream) {
+    if (!plan || !x || !out) return fail(SPA_ERR_INVALID, "NULL argument");
+    return qkv_call(plan, C, n_local_srcs(plan), x, w_packed, out, ws, stream, true);
+}
+
+spa_status spa_qkv_projection(spa_plan *plan, int C, int rank, const void *x, const void *w_packed, void *q, void *k,
+                              void *v, void *stream) {
+    SPA_TRY(qkv_check(plan, C));
+    if (plan->comm->kind == KIND_HOST) return fail(SPA_ERR_UNSUPPORTED, "host-only comm cannot execute");
+    if (rank < 0 || rank >= plan->P || (plan->comm->kind == KIND_NCCL && rank != plan->comm->rank))
+        return fail(SPA_ERR_INVALID, "bad rank");
+    for (const void *ptr : {x, w_packed, (const void *)q, (const void *)k, (const void *)v}) SPA_TRY(check_ptr(ptr, "pointer"));
+    SPA_CHECK_CUDA(cudaSetDevice(plan->comm->device));
+    const Split &s = plan->split;
+    plan->gemm_launches = 0;
+    for (int kh = 0; kh < s.G_h; ++kh) {   // head group kh: heads q*h + kh*g + jj of the [B, S_r, H, D] outputs
+        const long long off = (long long)kh * s.g * plan->sh.D * 2;
+        void *dst[3] = {(uint8_t *)q + off, (uint8_t *)k + off, (uint8_t *)v + off};
+        SPA_TRY(launch_qkv(plan, x, reinterpret_cast<const uint8_t *>(w_packed), C, rank, kh, dst,
+                           (long long)plan->h * plan->sh.D, (long long)plan->sh.H * plan->sh.D,
+                           reinterpret_cast<cudaStream_t>(stream)));
+    }
+    return SPA_OK;
 }
 
 // ------------------------------------------------------------------ ring attention (R21)

@@ -58,6 +58,28 @@ cudaError_t launch_lse_merge(const float *parts, long long part_stride, const fl
 
 cudaError_t launch_attention(const AttnProblem &p, cudaStream_t st);
 
+// QKV projection GEMM (qkv_gemm.cu): Y[m, n] = sum_k x[m, k] w[n, k] + bias[n] for
+// m < M, n < N, k < K (x [M][K], w [N][K] bf16 row-major, bias fp32 [N] or NULL); column n = (t*Q + q)*cols_per_q
+// + r (t < 3, cols_per_t = Q*cols_per_q) is stored as bf16 at dst[t] + q*q_stride + m*row_stride + r (elements).
+// N, cols_per_q multiples of 32; K multiple of 8; reserve_sms SMs are left free (communication kernels).
+struct QkvProblem {
+    const void *x, *w;
+    const float *bias;
+    int M, N, K;
+    void *dst[3];
+    long long q_stride, row_stride;
+    int cols_per_t, cols_per_q;
+    int reserve_sms;
+};
+struct QkvArgs {
+    int M, N, K, tiles_n, tiles;
+    const float *bias;
+    __nv_bfloat16 *dst[3];
+    long long q_stride, row_stride;
+    int cols_per_t, cols_per_q;
+};
+cudaError_t launch_qkv_gemm(const QkvProblem &p, cudaStream_t st);
+
 // Strided run copy: for (i3,i2,i1,i0) < count: copy run_bytes from
 // src + sum(i*src_stride) to dst + sum(i*dst_stride).  run_bytes % 64 == 0, 16-B aligned.
 struct CopyJob {

@@ -20,10 +20,11 @@ __all__ = [
     "spa_ring_attention", "spa_ring_attention_local", "spa_attention_host",
     "spa_reshard_seq_to_head", "spa_reshard_head_to_seq", "spa_reshard_seq_to_head_local",
     "spa_reshard_head_to_seq_local", "spa_pad_heads", "attention", "BUF_Q", "BUF_K", "BUF_V", "BUF_OUT",
-    "BUF_WS", "SPA_OPT_PROFILE", "SPA_OPT_SKIP_COMM", "SPA_OPT_COPROC_BUSY", "SPA_OPT_DIRECT",
+    "BUF_WS", "SPA_OPT_PROFILE", "SPA_OPT_SKIP_COMM", "SPA_OPT_COPROC_BUSY", "SPA_OPT_DIRECT", "SPA_OPT_COMM_SMS",
+    "spa_pipesp_qkv_attention", "spa_pipesp_qkv_attention_local", "spa_qkv_projection",
 ]
 
-SPA_OPT_PROFILE, SPA_OPT_SKIP_COMM, SPA_OPT_COPROC_BUSY, SPA_OPT_DIRECT = 1, 2, 3, 4
+SPA_OPT_PROFILE, SPA_OPT_SKIP_COMM, SPA_OPT_COPROC_BUSY, SPA_OPT_DIRECT, SPA_OPT_COMM_SMS = 1, 2, 3, 4, 5
 BUF_Q, BUF_K, BUF_V, BUF_OUT, BUF_WS = 0, 1, 2, 3, 4
 HEADER = os.path.join(os.path.dirname(_build.HERE), "include", "spa.h")
 
@@ -44,7 +45,7 @@ class Profile(ctypes.Structure):
     _fields_ = [("n_stages", ctypes.c_int), ("total_ms", ctypes.c_float), ("pack_ms", ctypes.c_float),
                 ("unpack_ms", ctypes.c_float), ("attn_ms", ctypes.c_float * 64),
                 ("a2a_in_ms", ctypes.c_float * 64), ("a2a_out_ms", ctypes.c_float * 64),
-                ("attn_launches", ctypes.c_int), ("copy_launches", ctypes.c_int)]
+                ("attn_launches", ctypes.c_int), ("copy_launches", ctypes.c_int), ("gemm_launches", ctypes.c_int)]
 
 
 class CopyDesc(ctypes.Structure):
@@ -125,6 +126,12 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "spa_plan_describe_unpack": ([_P, i, ctypes.POINTER(CopyDesc), i, ip], i),
         "spa_plan_describe_messages": ([_P, i, i, i, ctypes.POINTER(Msg), i, ip], i),
         "spa_plan_describe_attention": ([_P, i, i, ctypes.POINTER(AttnDesc)], i),
+        "spa_plan_qkv_weight_bytes": ([_P, i, ctypes.POINTER(ctypes.c_size_t)], i),
+        "spa_plan_qkv_workspace_bytes": ([_P, ctypes.POINTER(ctypes.c_size_t)], i),
+        "spa_plan_pack_qkv_weight": ([_P, i, _P, _P, _P, _P], i),
+        "spa_pipesp_qkv_attention": ([_P, i, _P, _P, _P, _P, _P], i),
+        "spa_pipesp_qkv_attention_local": ([_P, i, _PP, _P, _PP, _P, _P], i),
+        "spa_qkv_projection": ([_P, i, i, _P, _P, _P, _P, _P, _P], i),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -275,6 +282,31 @@ class Plan:
         import torch
         return torch.empty(max(self.workspace_bytes, 16), dtype=torch.uint8, device=device)
 
+    # -- QKV projection
+    def qkv_weight_bytes(self, C: int) -> int:
+        n = ctypes.c_size_t()
+        _check(load().spa_plan_qkv_weight_bytes(self.h, C, ctypes.byref(n)), "spa_plan_qkv_weight_bytes")
+        return n.value
+
+    @property
+    def qkv_workspace_bytes(self) -> int:
+        n = ctypes.c_size_t()
+        _check(load().spa_plan_qkv_workspace_bytes(self.h, ctypes.byref(n)), "spa_plan_qkv_workspace_bytes")
+        return n.value
+
+    def qkv_workspace(self, device="cuda"):
+        import torch
+        return torch.empty(max(self.qkv_workspace_bytes, 16), dtype=torch.uint8, device=device)
+
+    def pack_qkv_weight(self, w, bias=None, stream=None):
+        """w: bf16 [3*H*D, C] device tensor (fused nn.Linear weight), bias: fp32 [3*H*D] or None -> packed buffer."""
+        import torch
+        C = w.shape[1]
+        wp = torch.empty(self.qkv_weight_bytes(C), dtype=torch.uint8, device=w.device)
+        _check(load().spa_plan_pack_qkv_weight(self.h, C, _ptr(w), _ptr(bias), _ptr(wp), _stream(stream)),
+               "spa_plan_pack_qkv_weight")
+        return wp
+
     # -- host-side descriptions (no GPU needed)
     def describe_pack(self, rank: int) -> List[CopyDesc]:
         cap = 3 * self.comm.nranks * max(1, self.H) + 16
@@ -408,3 +440,18 @@ def spa_reshard_seq_to_head_local(plan: Plan, xs, x_heads, ws, stream=None):
 def spa_reshard_head_to_seq_local(plan: Plan, x_heads, xs, ws, stream=None):
     _check(load().spa_reshard_head_to_seq_local(plan.h, _arr(x_heads), _arr(xs), _ptr(ws), _stream(stream)),
            "spa_reshard_head_to_seq_local")
+
+
+def spa_pipesp_qkv_attention(plan: Plan, C: int, x, w_packed, out, ws, stream=None):
+    _check(load().spa_pipesp_qkv_attention(plan.h, C, _ptr(x), _ptr(w_packed), _ptr(out), _ptr(ws), _stream(stream)),
+           "spa_pipesp_qkv_attention")
+
+
+def spa_pipesp_qkv_attention_local(plan: Plan, C: int, xs, w_packed, outs, ws, stream=None):
+    _check(load().spa_pipesp_qkv_attention_local(plan.h, C, _arr(xs), _ptr(w_packed), _arr(outs), _ptr(ws),
+                                                 _stream(stream)), "spa_pipesp_qkv_attention_local")
+
+
+def spa_qkv_projection(plan: Plan, C: int, rank: int, x, w_packed, q, k, v, stream=None):
+    _check(load().spa_qkv_projection(plan.h, C, rank, _ptr(x), _ptr(w_packed), _ptr(q), _ptr(k), _ptr(v),
+                                     _stream(stream)), "spa_qkv_projection")
