@@ -10,6 +10,7 @@
 // N_st = 1 is Ulysses.  Stage k = (head group kh, query chunk c), k = kh*C + c.
 #include "../../include/spa.h"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -50,7 +51,7 @@ spa_status fail(spa_status s, const std::string &msg) {
         if (_s != SPA_OK) return _s;        \
     } while (0)
 
-enum Kind { KIND_NCCL = 0, KIND_LOOPBACK = 1, KIND_HOST = 2 };
+enum Kind { KIND_NCCL = 0, KIND_LOOPBACK = 1, KIND_HOST = 2, KIND_P2P = 3 };
 enum Buf { BUF_Q = 0, BUF_K = 1, BUF_V = 2, BUF_OUT = 3, BUF_WS = 4, BUF_XHEAD = 5 };
 
 long long align_up(long long x, long long a) { return (x + a - 1) / a * a; }
@@ -119,6 +120,14 @@ struct spa_plan {
     bool have_profile = false;
     int prof_stages = 0;   // stages the last profiled call executed (spa_profile.n_stages)
     std::map<std::string, int> prof_idx;
+    // P2P plans (KIND_P2P): every rank's workspace mapped into this process with CUDA IPC; per-call epoch
+    // flags in each workspace's tail order the cross-process exchange (ready[src], in[k][src], out[k][src], uint32)
+    std::vector<uint8_t *> peer_ws;   // [P]; own entry = the registered local workspace
+    std::vector<void *> ipc_bases;    // opened peer allocations (closed by spa_plan_destroy)
+    uint32_t epoch = 0;
+    long long off_flags = 0, off_outbuf = 0;
+    int n_flag_stages = 1;
+    bool p2p_flush = false;
     int attn_launches = 0, copy_launches = 0, gemm_launches = 0;
     cudaStream_t sc_alt = nullptr;  // second compute stream: odd stages, so stage k+1 fills stage k's wave tail
 };
@@ -383,6 +392,7 @@ uint8_t *resolve(const Exec &x, int rank, int buf, long long off) {
     int idx = (p->comm->kind == KIND_LOOPBACK) ? rank : 0;
     switch (buf) {
         case BUF_WS:
+            if (p->comm->kind == KIND_P2P) return p->peer_ws[rank] + off;   // own or a peer's (CUDA IPC mapping)
             return x.ptr.ws + (p->comm->kind == KIND_LOOPBACK ? (long long)rank * p->ws_rank_bytes : 0) + off;
         case BUF_XHEAD: return reinterpret_cast<uint8_t *>(x.ptr.xhead[idx]) + off;
         case BUF_OUT: return reinterpret_cast<uint8_t *>(x.ptr.out[idx]) + off;
@@ -392,10 +402,106 @@ uint8_t *resolve(const Exec &x, int rank, int buf, long long off) {
     }
 }
 
+// ------------------------------------------------------------------ P2P transport (CUDA IPC peer memory)
+// Driver stream memory operations order the cross-process exchange without any kernel spinning: the sender's
+// cuStreamWriteValue32 (with its implicit system-scope fence) stores the call's epoch into the receiver's flag
+// after the data, the receiver's stream waits with cuStreamWaitValue32(>= epoch) before using it.
+using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using AddrRangeFn = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+struct Drv {
+    WriteValue32Fn write32 = nullptr;
+    WaitValue32Fn wait32 = nullptr;
+    AddrRangeFn range = nullptr;
+};
+const Drv &drv() {
+    static const Drv d = [] {
+        Drv x;
+        auto get = [](const char *name) -> void * {
+            void *fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess)
+                return nullptr;
+            return fn;
+        };
+        x.write32 = reinterpret_cast<WriteValue32Fn>(get("cuStreamWriteValue32"));
+        x.wait32 = reinterpret_cast<WaitValue32Fn>(get("cuStreamWaitValue32"));
+        x.range = reinterpret_cast<AddrRangeFn>(get("cuMemGetAddressRange"));
+        return x;
+    }();
+    return d;
+}
+enum FlagKind { FLAG_READY = 0, FLAG_IN = 1, FLAG_OUT = 2 };
+int flag_slot(const spa_plan *p, int kind, int k, int src) {
+    return kind == FLAG_READY ? src : p->P + ((kind == FLAG_IN ? 0 : p->n_flag_stages) + k) * p->P + src;
+}
+long long flag_bytes(const spa_plan *p) { return 4LL * p->P * (1 + 2 * p->n_flag_stages); }
+// this rank's flag `kind/k` in the flag block of every other rank := epoch
+spa_status p2p_signal(spa_plan *p, cudaStream_t st, int kind, int k) {
+    const int me = p->comm->rank;
+    for (int q = 0; q < p->P; ++q) {
+        if (q == me) continue;
+        CUdeviceptr a = reinterpret_cast<CUdeviceptr>(p->peer_ws[q] + p->off_flags) + 4 * flag_slot(p, kind, k, me);
+        if (drv().write32(reinterpret_cast<CUstream>(st), a, p->epoch, 0) != CUDA_SUCCESS)
+            return fail(SPA_ERR_CUDA, "cuStreamWriteValue32 to a peer flag failed");
+    }
+    return SPA_OK;
+}
+// wait until every other rank's flag `kind/k` in this rank's flag block reached the epoch
+spa_status p2p_wait(spa_plan *p, cudaStream_t st, int kind, int k) {
+    const int me = p->comm->rank;
+    for (int src = 0; src < p->P; ++src) {
+        if (src == me) continue;
+        CUdeviceptr a = reinterpret_cast<CUdeviceptr>(p->peer_ws[me] + p->off_flags) + 4 * flag_slot(p, kind, k, src);
+        if (drv().wait32(reinterpret_cast<CUstream>(st), a, p->epoch,
+                         CU_STREAM_WAIT_VALUE_GEQ | (p->p2p_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0)) != CUDA_SUCCESS)
+            return fail(SPA_ERR_CUDA, "cuStreamWaitValue32 on a flag failed");
+    }
+    return SPA_OK;
+}
+// every rank has finished its previous call (its buffers may be written): a cross-process barrier on `st`
+spa_status p2p_barrier(spa_plan *p, cudaStream_t st) {
+    SPA_TRY(p2p_signal(p, st, FLAG_READY, 0));
+    return p2p_wait(p, st, FLAG_READY, 0);
+}
+
+template <class Gen>
+spa_status match_and_copy(Exec &x, int me, Gen gen, cudaStream_t st) {
+    // this rank's sends to q matched with q's receives from this rank, in order (NCCL semantics); copy-engine
+    // copies straight into the peer's receive region (no SMs taken from the attention)
+    spa_plan *p = x.p;
+    std::vector<Msg> mine;
+    gen(me, mine);
+    for (int q = 0; q < p->P; ++q) {
+        std::vector<Msg> theirs;
+        gen(q, theirs);
+        std::vector<const Msg *> sends, recvs;
+        for (const Msg &g : mine) if (!g.is_recv && g.peer == q) sends.push_back(&g);
+        for (const Msg &g : theirs) if (g.is_recv && g.peer == me) recvs.push_back(&g);
+        if (sends.size() != recvs.size()) return fail(SPA_ERR_COMM, "p2p: unmatched messages");
+        for (size_t i = 0; i < sends.size(); ++i) {
+            if (sends[i]->bytes != recvs[i]->bytes) return fail(SPA_ERR_COMM, "p2p: size mismatch");
+            SPA_CHECK_CUDA(cudaMemcpyAsync(resolve(x, q, recvs[i]->buf, recvs[i]->off),
+                                           resolve(x, me, sends[i]->buf, sends[i]->off), (size_t)sends[i]->bytes,
+                                           cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    return SPA_OK;
+}
+
 // Issue one stage exchange (dir 0 in, 1 out) on the comm stream.
 spa_status run_exchange(Exec &x, int k, int dir) {
     spa_plan *p = x.p;
     if (p->skip_comm) return SPA_OK;
+    if (p->comm->kind == KIND_P2P) {
+        auto gen = [&](int r, std::vector<Msg> &m) {
+            if (dir == 0) gen_in_msgs(p, *x.s, k, r, x.in_tensors, x.q_recv_buf, m);
+            else gen_out_msgs(p, *x.s, k, r, x.o_send_buf, m);
+        };
+        SPA_TRY(match_and_copy(x, p->comm->rank, gen, x.sm));
+        return p2p_signal(p, x.sm, dir == 0 ? FLAG_IN : FLAG_OUT, k);
+    }
     if (p->comm->kind == KIND_NCCL) {
         std::vector<Msg> m;
         if (dir == 0) gen_in_msgs(p, *x.s, k, p->comm->rank, x.in_tensors, x.q_recv_buf, m);
@@ -630,6 +736,120 @@ spa_status execute_direct(Exec &x) {
     return SPA_OK;
 }
 
+// Direct transport across processes (SURVEY f1 over NVLink / CUDA IPC): this rank's pack stores its runs straight
+// into the owners' receive regions (peer pointers), its attention epilogues store every output row straight into the
+// source rank's output landing buffer (ws region `outbuf`, [B, S_r, H, D], Psi_g fused), and each source copies its
+// landing buffer to `out` once every owner signalled.  Same jobs / row tables as the loopback model above, with the
+// peers' workspaces instead of local ones, and epoch flags instead of stream order.
+spa_status execute_direct_p2p(Exec &x) {
+    spa_plan *p = x.p;
+    const Split &s = *x.s;
+    const int N = s.n(), me = p->comm->rank;
+    const long long D2 = (long long)p->sh.D * 2, H = p->sh.H, run = s.g * D2;
+    Prof pr{p};
+    ++p->epoch;
+    pr.begin("total", x.sc);
+    SPA_TRY(p2p_barrier(p, x.sc));   // the pack below writes into the peers' receive regions
+    pr.begin("pack", x.sc);
+    std::vector<CopyJob> jobs;
+    const long long offs[3] = {p->off_recvQ, p->off_recvK, p->off_recvV};
+    if (is_source(p, me)) {
+        const void *xs[3] = {x.ptr.q[0], x.ptr.k[0], x.ptr.v[0]};
+        const long long n = p->len[me];
+        for (int t = 0; t < 3; ++t)
+            for (int kh = 0; kh < s.G_h; ++kh)
+                for (int q = 0; q < p->P; ++q) {
+                    const int nreal = real_heads(p, s, q, kh);
+                    if (nreal == 0) continue;
+                    const uint8_t *src = reinterpret_cast<const uint8_t *>(xs[t]) + (q * p->h + kh * s.g) * D2;
+                    uint8_t *wq = resolve(x, q, BUF_WS, offs[t]);
+                    CopyJob j{};
+                    j.count[0] = j.count[1] = 1;
+                    j.count[2] = p->sh.B;
+                    j.src_stride[2] = n * H * D2; j.src_stride[3] = H * D2;
+                    j.dst_stride[3] = run;
+                    j.run_bytes = nreal * D2;
+                    if (t == 0) {
+                        for (int c = 0; c < s.C; ++c) {
+                            const long long L = Lsrc(p, s, me, c);
+                            if (L == 0) continue;
+                            CopyJob jc = j;
+                            jc.src = src + clo(p, s, me, c) * H * D2;
+                            jc.dst = wq + idx_qo(p, s, kh, c, 0, me) * 2;
+                            jc.count[3] = L;
+                            jc.dst_stride[2] = Lstage(p, s, c) * run;
+                            jobs.push_back(jc);
+                        }
+                    } else {
+                        j.src = src;
+                        j.dst = wq + idx_kv(p, s, kh, 0, me) * 2;
+                        j.count[3] = n;
+                        j.dst_stride[2] = (long long)p->sh.S * run;
+                        jobs.push_back(j);
+                    }
+                }
+    }
+    if (!jobs.empty()) SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sc, &p->copy_launches));
+    pr.end("pack", x.sc);
+    if (!p->skip_comm) {
+        SPA_TRY(p2p_signal(p, x.sc, FLAG_IN, 0));   // all of this rank's runs are in place (every stage)
+        SPA_TRY(p2p_wait(p, x.sc, FLAG_IN, 0));
+    }
+    if (!p->sc_alt) SPA_CHECK_CUDA(cudaStreamCreateWithFlags(&p->sc_alt, cudaStreamNonBlocking));
+    cudaEvent_t ev_pack = p->sync_ev[1], ev_alt = p->sync_ev[2];
+    SPA_CHECK_CUDA(cudaEventRecord(ev_pack, x.sc));
+    SPA_CHECK_CUDA(cudaStreamWaitEvent(p->sc_alt, ev_pack, 0));
+    for (int k = 0; k < N; ++k) {
+        const int kh = k / s.C, c = k % s.C;
+        const long long Lst = Lstage(p, s, c);
+        const std::string an = "attn" + std::to_string(k);
+        cudaStream_t st = (k & 1) ? p->sc_alt : x.sc;
+        pr.begin(an, st);
+        const int nreal = real_heads(p, s, me, kh);
+        if (nreal > 0) {
+            uint8_t *ws = resolve(x, me, BUF_WS, 0);
+            AttnProblem a{};
+            a.q = ws + p->off_recvQ + base_stage(p, s, kh, c) * 2;
+            a.k = ws + p->off_recvK + idx_kv(p, s, kh, 0, 0) * 2;
+            a.v = ws + p->off_recvV + idx_kv(p, s, kh, 0, 0) * 2;
+            a.o = ws + p->off_O;
+            a.B = p->sh.B; a.Sq = (int)Lst; a.Skv = p->sh.S; a.n_heads = nreal; a.D = p->sh.D;
+            a.kv_len = p->kv_len;
+            a.q_tok_stride = a.kv_tok_stride = (long long)s.g * p->sh.D;
+            a.q_batch_stride = Lst * s.g * p->sh.D;
+            a.kv_batch_stride = (long long)p->sh.S * s.g * p->sh.D;
+            a.o_tok_stride = H * p->sh.D;
+            a.o_batch_stride = 0;
+            a.n_dst = p->Psrc;
+            for (int q = 0; q < p->Psrc; ++q) {
+                a.row_begin[q] = (int)src_prefix(p, s, c, q);
+                a.dst[q] = resolve(x, q, BUF_WS, p->off_outbuf) +
+                           ((clo(p, s, q, c) * H) + (long long)me * p->h + (long long)kh * s.g) * D2;
+                a.dst_batch_stride[q] = (long long)p->len[q] * H * p->sh.D;
+            }
+            a.row_begin[p->Psrc] = (int)Lst;
+            SPA_CHECK_CUDA(launch_attention(a, st));
+            ++p->attn_launches;
+        }
+        pr.end(an, st);
+    }
+    SPA_CHECK_CUDA(cudaEventRecord(ev_alt, p->sc_alt));
+    SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_alt, 0));
+    if (!p->skip_comm) {
+        SPA_TRY(p2p_signal(p, x.sc, FLAG_OUT, 0));   // this owner's rows are in every source's landing buffer
+        SPA_TRY(p2p_wait(p, x.sc, FLAG_OUT, 0));
+    }
+    if (is_source(p, me)) {
+        pr.begin("unpack", x.sc);
+        SPA_CHECK_CUDA(cudaMemcpyAsync(x.ptr.out[0], resolve(x, me, BUF_WS, p->off_outbuf),
+                                       (size_t)p->sh.B * p->len[me] * H * D2, cudaMemcpyDeviceToDevice, x.sc));
+        pr.end("unpack", x.sc);
+    }
+    pr.end("total", x.sc);
+    finish_profile(p, pr, N);
+    return SPA_OK;
+}
+
 // The whole call: single-rank fast path, else the staged pipeline.
 spa_status execute(Exec &x) {
     spa_plan *p = x.p;
@@ -639,7 +859,8 @@ spa_status execute(Exec &x) {
     const Split &s = *x.s;
     const int N = s.n();
     SPA_TRY(ensure_events(p, 4 + 3 * (size_t)N + s.G_h, p->profile ? 8 + 6 * (size_t)N : 0));
-    if (p->direct && p->P > 1 && x.has_attn && x.has_pack && x.has_out && !x.qkv) return execute_direct(x);
+    if (p->direct && p->P > 1 && x.has_attn && x.has_pack && x.has_out && !x.qkv)
+        return p->comm->kind == KIND_P2P ? execute_direct_p2p(x) : execute_direct(x);
     Prof pr{p};
     if (p->P == 1) {
         // one rank owns everything: attention straight on the caller's [B,S,H,D] buffers
@@ -689,6 +910,11 @@ spa_status execute(Exec &x) {
     pr.begin("total", x.sc);
     SPA_CHECK_CUDA(cudaEventRecord(ev_entry, x.sc));
     SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_entry, 0));
+    const bool p2p = p->comm->kind == KIND_P2P;
+    if (p2p) {   // a new epoch; no rank writes into a peer before that peer finished its previous call
+        ++p->epoch;
+        SPA_TRY(p2p_barrier(p, x.sm));
+    }
     if (x.has_pack) {
         pr.begin("pack", x.sc);
         if (x.qkv) SPA_TRY(run_qkv_pack(x, ev_gemm));
@@ -714,6 +940,7 @@ spa_status execute(Exec &x) {
         for (int k = 0; k < N; ++k) {
             cudaStream_t st = (k & 1) ? x.sc_alt : x.sc;
             SPA_CHECK_CUDA(cudaStreamWaitEvent(st, ev_in[k], 0));
+            if (p2p && !p->skip_comm) SPA_TRY(p2p_wait(p, st, FLAG_IN, k));   // the peers' pieces of stage k
             const std::string an = "attn" + std::to_string(k);
             pr.begin(an, st);
             SPA_TRY(run_attention(x, k, st));
@@ -728,6 +955,8 @@ spa_status execute(Exec &x) {
             if (k + 2 < N) SPA_TRY(issue_in(k + 2));
         }
         SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_out[N - 1], 0));
+        if (p2p && !p->skip_comm)
+            for (int k = 0; k < N; ++k) SPA_TRY(p2p_wait(p, x.sc, FLAG_OUT, k));   // every owner's output rows
     } else if (!x.has_out) {
         // reshard seq->head: the one input exchange only
         SPA_TRY(issue_in(0));
@@ -765,6 +994,10 @@ spa_status prepare(spa_plan *p, Exec &x, void *ws, void *stream, bool local) {
     if (local != (p->comm->kind == KIND_LOOPBACK))
         return fail(SPA_ERR_INVALID, local ? "*_local calls need a loopback plan" : "loopback plans need the *_local calls");
     if (p->P > 1) SPA_TRY(check_ptr(ws, "ws"));
+    if (p->comm->kind == KIND_P2P && p->P > 1) {
+        if (p->peer_ws.empty()) return fail(SPA_ERR_INVALID, "p2p plan: call spa_plan_ipc_open first");
+        if (ws != p->peer_ws[p->comm->rank]) return fail(SPA_ERR_INVALID, "p2p plan: ws is not the registered workspace");
+    }
     x.p = p;
     x.ptr.ws = reinterpret_cast<uint8_t *>(ws);
     x.sc = reinterpret_cast<cudaStream_t>(stream);
@@ -955,6 +1188,77 @@ spa_status spa_comm_init_loopback(spa_comm **comm, int nvirtual, int device) {
     return SPA_OK;
 }
 
+spa_status spa_comm_init_p2p(spa_comm **comm, int nranks, int rank, int device) {
+    if (!comm || nranks < 1 || rank < 0 || rank >= nranks) return fail(SPA_ERR_INVALID, "bad p2p comm arguments");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return fail(SPA_ERR_CUDA, "no such CUDA device");
+    if (!drv().write32 || !drv().wait32 || !drv().range)
+        return fail(SPA_ERR_UNSUPPORTED, "driver lacks stream memory operations");
+    spa_comm *c = new spa_comm;
+    c->kind = KIND_P2P; c->nranks = nranks; c->rank = rank; c->device = device;
+    *comm = c;
+    return SPA_OK;
+}
+
+spa_status spa_plan_ipc_handle(spa_plan *plan, void *ws, uint8_t handle[SPA_IPC_HANDLE_BYTES]) {
+    if (!plan || !ws || !handle) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (plan->comm->kind != KIND_P2P) return fail(SPA_ERR_INVALID, "not a p2p plan");
+    SPA_CHECK_CUDA(cudaSetDevice(plan->comm->device));
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (drv().range(&base, &size, reinterpret_cast<CUdeviceptr>(ws)) != CUDA_SUCCESS)
+        return fail(SPA_ERR_INVALID, "ws is not device memory");
+    size_t need = 0;
+    SPA_TRY(spa_plan_workspace_bytes(plan, &need));
+    const unsigned long long off = reinterpret_cast<CUdeviceptr>(ws) - base;
+    if (off + need > size) return fail(SPA_ERR_INVALID, "ws allocation smaller than the plan's workspace");
+    cudaIpcMemHandle_t h;
+    SPA_CHECK_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base)));
+    static_assert(sizeof(h) + 8 == SPA_IPC_HANDLE_BYTES, "handle size");
+    memcpy(handle, &h, sizeof(h));
+    memcpy(handle + sizeof(h), &off, 8);
+    return SPA_OK;
+}
+
+spa_status spa_plan_ipc_open(spa_plan *plan, void *ws, const uint8_t *handles) {
+    if (!plan || !ws || !handles) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (plan->comm->kind != KIND_P2P) return fail(SPA_ERR_INVALID, "not a p2p plan");
+    if (!plan->peer_ws.empty()) return fail(SPA_ERR_INVALID, "p2p plan already opened");
+    SPA_CHECK_CUDA(cudaSetDevice(plan->comm->device));
+    const int me = plan->comm->rank;
+    std::vector<uint8_t *> peers(plan->P, nullptr);
+    for (int q = 0; q < plan->P; ++q) {
+        if (q == me) {
+            peers[q] = reinterpret_cast<uint8_t *>(ws);
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        unsigned long long off = 0;
+        memcpy(&h, handles + (size_t)q * SPA_IPC_HANDLE_BYTES, sizeof(h));
+        memcpy(&off, handles + (size_t)q * SPA_IPC_HANDLE_BYTES + sizeof(h), 8);
+        void *base = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            for (void *b : plan->ipc_bases) cudaIpcCloseMemHandle(b);
+            plan->ipc_bases.clear();
+            return fail(SPA_ERR_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+        }
+        peers[q] = reinterpret_cast<uint8_t *>(base) + off;
+        plan->ipc_bases.push_back(base);
+    }
+    int flush = 0;
+    if (cudaDeviceGetAttribute(&flush, static_cast<cudaDeviceAttr>(CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES),
+                               plan->comm->device) == cudaSuccess)
+        plan->p2p_flush = flush != 0;
+    cudaGetLastError();
+    plan->peer_ws = peers;
+    plan->epoch = 0;
+    // this rank's flags start at 0 (the caller synchronises all ranks after ipc_open, before the first call)
+    SPA_CHECK_CUDA(cudaMemset(reinterpret_cast<uint8_t *>(ws) + plan->off_flags, 0, (size_t)flag_bytes(plan)));
+    return SPA_OK;
+}
+
 spa_status spa_comm_init_host(spa_comm **comm, int nranks, int rank) {
     if (!comm || nranks < 1 || rank < 0 || rank >= nranks) return fail(SPA_ERR_INVALID, "bad host comm arguments");
     spa_comm *c = new spa_comm;
@@ -1025,6 +1329,7 @@ spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *sha
     if (s.ulysses < 0 || (!s.ring && s.ulysses > 1)) return fail(SPA_ERR_INVALID, "ulysses degree needs ring = 1");
     if (s.ring && (s.stages != 1 || s.pad_heads != 0))
         return fail(SPA_ERR_INVALID, "ring / USP plans take stages = 1 and pad_heads = 0");
+    if (s.ring && comm->kind == KIND_P2P) return fail(SPA_ERR_UNSUPPORTED, "ring / USP plans need an NCCL or loopback comm");
     if (s.ring && s.ulysses > 1) return create_usp_plan(plan, comm, s);
     if (s.ring) {
         // Ring attention: every rank keeps all heads; only S % P matters.
@@ -1075,6 +1380,11 @@ spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *sha
         p->off_orecv = take(p->E_src);
         p->off_recvQ = take(p->E_own); p->off_recvK = take(p->E_own); p->off_recvV = take(p->E_own);
         p->off_O = take(p->E_own);
+        if (comm->kind == KIND_P2P) {   // epoch flags + the direct transport's output landing buffer
+            p->n_flag_stages = p->split.n();
+            p->off_flags = take((flag_bytes(p) + 1) / 2);
+            p->off_outbuf = take((long long)s.B * p->S_l * s.H * s.D);
+        }
         p->ws_rank_bytes = off;
     }
     *plan = p;
@@ -1106,6 +1416,7 @@ spa_status spa_plan_destroy(spa_plan *plan) {
     spa_plan_destroy(plan->ring_plan);
     if (plan->uly_comm) spa_comm_destroy(plan->uly_comm);
     if (plan->ring_comm) spa_comm_destroy(plan->ring_comm);
+    for (void *b : plan->ipc_bases) cudaIpcCloseMemHandle(b);
     for (auto e : plan->sync_ev) cudaEventDestroy(e);
     for (auto e : plan->prof_ev) cudaEventDestroy(e);
     if (plan->sc_alt) cudaStreamDestroy(plan->sc_alt);
@@ -1474,6 +1785,8 @@ static spa_status ring_call(spa_plan *p, int n, const void *const q[], const voi
 static spa_status reshard_call(spa_plan *plan, int n, const void *const x[], void *const xh[], void *ws, void *stream,
                                bool local, bool to_head) {
     if (plan && plan->ring) return fail(SPA_ERR_INVALID, "ring plan: no reshard");
+    if (plan && plan->comm->kind == KIND_P2P)   // the receive side is the caller's x_head, not a mapped workspace
+        return fail(SPA_ERR_UNSUPPORTED, "p2p plans: reshard calls need an NCCL or loopback comm");
     Exec e{};
     SPA_TRY(prepare(plan, e, ws, stream, local));
     if (plan->Psrc != plan->P) return fail(SPA_ERR_INVALID, "reshard needs n_src == nranks");
