@@ -71,6 +71,15 @@ spa_status spa_comm_init(spa_comm **comm, const uint8_t id[128], int nranks, int
 /* `nvirtual` virtual ranks on ONE GPU (tests / single-GPU measurement): the all-to-all
  * becomes device-to-device copies on the comm stream, everything else is identical. */
 spa_status spa_comm_init_loopback(spa_comm **comm, int nvirtual, int device);
+/* One process per GPU WITHOUT NCCL: the exchange runs over CUDA IPC peer memory (NVLink / NVSwitch between GPUs;
+ * also valid for several processes sharing one GPU) -- SURVEY f1, DESIGN.md §6.  Every rank's workspace is mapped
+ * into every other rank (spa_plan_ipc_handle / spa_plan_ipc_open below); the staged exchange is copy-engine
+ * cudaMemcpyAsync of each message straight into the receiver's region (no SMs taken from the attention), and
+ * SPA_OPT_DIRECT makes the pack kernel and the attention epilogue store to the peers themselves.  Cross-process
+ * order: per-call epoch flags in each workspace's tail, written with cuStreamWriteValue32 (system-scope fence
+ * first) after the data and awaited with cuStreamWaitValue32 -- no kernel ever spins on a flag.  Ulysses / PipeSP /
+ * Aco / QKV plans; no ring or reshard calls.  `rank` and `nranks` come from the caller's launcher. */
+spa_status spa_comm_init_p2p(spa_comm **comm, int nranks, int rank, int device);
 /* Host-only rank group: plans can be created, validated and described (spa_plan_describe_*),
  * but not executed.  Used to test the multi-rank host logic without a GPU. */
 spa_status spa_comm_init_host(spa_comm **comm, int nranks, int rank);
@@ -81,7 +90,7 @@ spa_status spa_comm_split(spa_comm *comm, int color, int key, spa_comm **sub);
 spa_status spa_comm_check(spa_comm *comm);
 spa_status spa_comm_destroy(spa_comm *comm);
 /* rank count / own rank (-1 for loopback, which holds all ranks). */
-spa_status spa_comm_info(const spa_comm *comm, int *nranks, int *rank, int *kind /* 0 nccl,1 loopback,2 host */);
+spa_status spa_comm_info(const spa_comm *comm, int *nranks, int *rank, int *kind /* 0 nccl,1 loopback,2 host,3 p2p */);
 
 /* ------------------------------------------------------------------ plans */
 typedef struct {
@@ -118,6 +127,17 @@ spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *sha
 /* Device workspace bytes the caller must pass as `ws` (per rank; for loopback plans:
  * for all virtual ranks together).  Zero when nranks == 1. */
 spa_status spa_plan_workspace_bytes(const spa_plan *plan, size_t *bytes);
+/* P2P plans (spa_comm_init_p2p): register the workspace the calls will pass (device memory of at least
+ * spa_plan_workspace_bytes(); e.g. a torch tensor).  Collective set-up, once per plan:
+ *   1. every rank: spa_plan_ipc_handle(plan, ws, handle)   -- SPA_IPC_HANDLE_BYTES bytes (CUDA IPC handle of the
+ *      allocation holding ws + the offset of ws in it)
+ *   2. the caller gathers all ranks' handles in rank order (e.g. torch.distributed.all_gather_object)
+ *   3. every rank: spa_plan_ipc_open(plan, ws, handles)    -- maps the peers' workspaces, zeroes this rank's flags
+ *   4. a host barrier over all ranks (so that no flag is written before its owner zeroed it)
+ * Afterwards every call must pass this same ws; spa_plan_destroy unmaps the peers. */
+#define SPA_IPC_HANDLE_BYTES 72
+spa_status spa_plan_ipc_handle(spa_plan *plan, void *ws, uint8_t handle[SPA_IPC_HANDLE_BYTES]);
+spa_status spa_plan_ipc_open(spa_plan *plan, void *ws, const uint8_t *handles);
 /* G_h, C, g of the plan's stage split. */
 spa_status spa_plan_stage_split(const spa_plan *plan, int *G_h, int *C, int *g);
 spa_status spa_plan_destroy(spa_plan *plan);

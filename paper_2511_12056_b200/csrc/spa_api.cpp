@@ -1509,7 +1509,7 @@ spa_status spa_aco_attention(spa_plan *plan, const void *q, const void *k, const
     // no co-processor ranks (N_decode = 0): Aco is PipeSP on all ranks
     if (plan->Psrc == plan->P) return attention_call(plan, 1, &q, &k, &v, &out, ws, stream, false, false);
     if (plan->coproc_busy) return fail(SPA_ERR_BUSY, "co-processor group busy");
-    const bool src = plan->comm->kind == KIND_NCCL && is_source(plan, plan->comm->rank);
+    const bool src = plan->comm->kind != KIND_LOOPBACK && is_source(plan, plan->comm->rank);
     if (!src) {
         if (q || k || v || out) return fail(SPA_ERR_INVALID, "co-processor ranks pass NULL q/k/v/out");
         Exec x{};

@@ -95,6 +95,9 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "spa_comm_init": ([_PP, ctypes.c_char_p, i, i, i], i),
         "spa_comm_init_loopback": ([_PP, i, i], i),
         "spa_comm_init_host": ([_PP, i, i], i),
+        "spa_comm_init_p2p": ([_PP, i, i, i], i),
+        "spa_plan_ipc_handle": ([_P, _P, ctypes.c_char_p], i),
+        "spa_plan_ipc_open": ([_P, _P, ctypes.c_char_p], i),
         "spa_comm_split": ([_P, i, i, _PP], i),
         "spa_comm_check": ([_P], i),
         "spa_comm_destroy": ([_P], i),
@@ -216,6 +219,13 @@ class Comm:
         return cls(h.value)
 
     @classmethod
+    def p2p(cls, nranks: int, rank: int, device: int) -> "Comm":
+        """One process per rank, exchange over CUDA IPC peer memory (no NCCL); see Plan.ipc_setup."""
+        h = ctypes.c_void_p()
+        _check(load().spa_comm_init_p2p(ctypes.byref(h), nranks, rank, device), "spa_comm_init_p2p")
+        return cls(h.value)
+
+    @classmethod
     def host(cls, nranks: int, rank: int) -> "Comm":
         h = ctypes.c_void_p()
         _check(load().spa_comm_init_host(ctypes.byref(h), nranks, rank), "spa_comm_init_host")
@@ -281,6 +291,27 @@ class Plan:
     def workspace(self, device="cuda"):
         import torch
         return torch.empty(max(self.workspace_bytes, 16), dtype=torch.uint8, device=device)
+
+    # -- P2P plans (CUDA IPC): register the workspace the calls will use
+    IPC_HANDLE_BYTES = 72
+
+    def ipc_handle(self, ws) -> bytes:
+        buf = ctypes.create_string_buffer(self.IPC_HANDLE_BYTES)
+        _check(load().spa_plan_ipc_handle(self.h, _ptr(ws), buf), "spa_plan_ipc_handle")
+        return buf.raw
+
+    def ipc_open(self, ws, handles: Sequence[bytes]):
+        blob = b"".join(handles)
+        assert len(blob) == self.IPC_HANDLE_BYTES * self.comm.nranks
+        _check(load().spa_plan_ipc_open(self.h, _ptr(ws), blob), "spa_plan_ipc_open")
+
+    def ipc_setup(self, ws, group=None):
+        """Collective: exchange the IPC handles of every rank's ws over torch.distributed and map them."""
+        import torch.distributed as dist
+        hs = [None] * self.comm.nranks
+        dist.all_gather_object(hs, self.ipc_handle(ws), group=group)
+        self.ipc_open(ws, hs)
+        dist.barrier(group=group)
 
     # -- QKV projection (SURVEY f3)
     def qkv_weight_bytes(self, C: int) -> int:

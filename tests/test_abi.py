@@ -223,3 +223,13 @@ def test_plain_c_client(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=60)
     assert out.returncode == 0, out.stderr
     assert "c abi ok" in out.stdout
+
+
+def test_p2p_comm_needs_a_device():
+    """spa_comm_init_p2p (CUDA IPC transport) fails cleanly without a GPU: SPA_ERR_CUDA, nothing created."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by tests/test_gpu_p2p.py")
+    with pytest.raises(spa.SpaError) as e:
+        spa.Comm.p2p(2, 0, 0)
+    assert e.value.status == 4
