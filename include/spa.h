@@ -68,6 +68,20 @@ typedef struct spa_plan spa_plan;
 spa_status spa_get_unique_id(uint8_t id[128]);
 /* One process per GPU: NCCL communicator of `nranks` ranks over NVLink/NVSwitch; `device` = CUDA ordinal. */
 spa_status spa_comm_init(spa_comm **comm, const uint8_t id[128], int nranks, int rank, int device);
+/* The same with NCCL communicator settings: the SM budget of NCCL's kernels while the attention grid occupies the
+ * GPU (ncclConfig_t minCTAs / maxCTAs / CTAPolicy; NCCL 2.28).  0 leaves a field at NCCL's default (and its env
+ * variables, e.g. NCCL_MAX_CTAS, apply).  cta_policy: 0 default, 1 efficiency, 2 zero-CTA (copy engines, for
+ * buffers NCCL supports it on). */
+typedef struct {
+    int min_ctas, max_ctas, cta_policy;
+} spa_comm_config;
+spa_status spa_comm_init_config(spa_comm **comm, const uint8_t id[128], int nranks, int rank, int device,
+                                const spa_comm_config *cfg);
+/* Failure handling: waits until `stream` completes, polling the communicator's asynchronous error state.  A peer
+ * failure (NCCL async error) or no completion within timeout_ms (< 0: no limit) ABORTS the NCCL communicator
+ * (ncclCommAbort unblocks this rank's pending NCCL kernels) and returns SPA_ERR_COMM; the comm can then only be
+ * destroyed.  Returns SPA_OK when the stream completed, SPA_ERR_CUDA on a CUDA fault. */
+spa_status spa_comm_wait(spa_comm *comm, void *stream, int timeout_ms);
 /* `nvirtual` virtual ranks on ONE GPU (tests / single-GPU measurement): the all-to-all
  * becomes device-to-device copies on the comm stream, everything else is identical. */
 spa_status spa_comm_init_loopback(spa_comm **comm, int nvirtual, int device);

@@ -15,11 +15,13 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <map>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "spa_internal.h"
@@ -1164,13 +1166,29 @@ spa_status spa_get_unique_id(uint8_t id[128]) {
 }
 
 spa_status spa_comm_init(spa_comm **comm, const uint8_t id[128], int nranks, int rank, int device) {
+    return spa_comm_init_config(comm, id, nranks, rank, device, nullptr);
+}
+
+spa_status spa_comm_init_config(spa_comm **comm, const uint8_t id[128], int nranks, int rank, int device,
+                                const spa_comm_config *cfg) {
     if (!comm || !id) return fail(SPA_ERR_INVALID, "NULL argument");
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SPA_ERR_INVALID, "bad rank/nranks");
+    if (cfg && (cfg->min_ctas < 0 || cfg->max_ctas < 0 || (cfg->max_ctas && cfg->min_ctas > cfg->max_ctas)))
+        return fail(SPA_ERR_INVALID, "bad CTA bounds");
+    if (cfg && (cfg->cta_policy < 0 || cfg->cta_policy > 2)) return fail(SPA_ERR_INVALID, "bad CTA policy");
     SPA_CHECK_CUDA(cudaSetDevice(device));
     ncclUniqueId u;
     memcpy(u.internal, id, 128);
     ncclComm_t nc;
-    SPA_CHECK_NCCL(ncclCommInitRank(&nc, nranks, u, rank));
+    ncclConfig_t nccfg = NCCL_CONFIG_INITIALIZER;
+    // SM budget of NCCL's kernels while the attention grid occupies the GPU (NCCL's own env variables,
+    // e.g. NCCL_MAX_CTAS, still apply when a field is left at 0)
+    if (cfg) {
+        if (cfg->min_ctas) nccfg.minCTAs = cfg->min_ctas;
+        if (cfg->max_ctas) nccfg.maxCTAs = cfg->max_ctas;
+        if (cfg->cta_policy) nccfg.CTAPolicy = cfg->cta_policy;
+    }
+    SPA_CHECK_NCCL(ncclCommInitRankConfig(&nc, nranks, u, rank, &nccfg));
     spa_comm *c = new spa_comm;
     c->kind = KIND_NCCL; c->nranks = nranks; c->rank = rank; c->device = device; c->nccl = nc;
     *comm = c;
@@ -1294,6 +1312,39 @@ spa_status spa_comm_check(spa_comm *comm) {
     if (comm->kind != KIND_HOST) {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(SPA_ERR_CUDA, cudaGetErrorString(e));
+    }
+    return SPA_OK;
+}
+
+spa_status spa_comm_wait(spa_comm *comm, void *stream, int timeout_ms) {
+    if (!comm) return fail(SPA_ERR_INVALID, "comm is NULL");
+    if (comm->kind == KIND_HOST) return fail(SPA_ERR_UNSUPPORTED, "host-only comm");
+    SPA_CHECK_CUDA(cudaSetDevice(comm->device));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        cudaError_t q = cudaStreamQuery(st);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) return fail(SPA_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(q));
+        if (comm->kind == KIND_NCCL) {
+            ncclResult_t a = ncclSuccess;
+            SPA_CHECK_NCCL(ncclCommGetAsyncError(comm->nccl, &a));
+            if (a != ncclSuccess && a != ncclInProgress) {
+                ncclCommAbort(comm->nccl);   // a peer failed: unblock this rank's kernels
+                comm->nccl = nullptr;
+                return fail(SPA_ERR_COMM, std::string("communicator failed, aborted: ") + ncclGetErrorString(a));
+            }
+        }
+        const long long ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+        if (timeout_ms >= 0 && ms > timeout_ms) {
+            if (comm->kind == KIND_NCCL && comm->nccl) {
+                ncclCommAbort(comm->nccl);
+                comm->nccl = nullptr;
+                return fail(SPA_ERR_COMM, "timeout: communicator aborted (a peer stopped participating)");
+            }
+            return fail(SPA_ERR_COMM, "timeout waiting for the stream");
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
     }
     return SPA_OK;
 }

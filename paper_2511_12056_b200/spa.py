@@ -41,6 +41,10 @@ class Shape(ctypes.Structure):
                 ("ring", ctypes.c_int), ("ulysses", ctypes.c_int)]
 
 
+class CommConfig(ctypes.Structure):
+    _fields_ = [("min_ctas", ctypes.c_int), ("max_ctas", ctypes.c_int), ("cta_policy", ctypes.c_int)]
+
+
 class Profile(ctypes.Structure):
     _fields_ = [("n_stages", ctypes.c_int), ("total_ms", ctypes.c_float), ("pack_ms", ctypes.c_float),
                 ("unpack_ms", ctypes.c_float), ("attn_ms", ctypes.c_float * 64),
@@ -96,6 +100,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "spa_comm_init_loopback": ([_PP, i, i], i),
         "spa_comm_init_host": ([_PP, i, i], i),
         "spa_comm_init_p2p": ([_PP, i, i, i], i),
+        "spa_comm_init_config": ([_PP, ctypes.c_char_p, i, i, i, ctypes.POINTER(CommConfig)], i),
+        "spa_comm_wait": ([_P, _P, i], i),
         "spa_plan_ipc_handle": ([_P, _P, ctypes.c_char_p], i),
         "spa_plan_ipc_open": ([_P, _P, ctypes.c_char_p], i),
         "spa_comm_split": ([_P, i, i, _PP], i),
@@ -207,10 +213,20 @@ class Comm:
         self.nranks, self.rank, self.kind = n.value, r.value, k.value
 
     @classmethod
-    def nccl(cls, uid: bytes, nranks: int, rank: int, device: int) -> "Comm":
+    def nccl(cls, uid: bytes, nranks: int, rank: int, device: int, min_ctas: int = 0, max_ctas: int = 0,
+             cta_policy: int = 0) -> "Comm":
         h = ctypes.c_void_p()
-        _check(load().spa_comm_init(ctypes.byref(h), uid, nranks, rank, device), "spa_comm_init")
+        if min_ctas or max_ctas or cta_policy:
+            cfg = CommConfig(min_ctas, max_ctas, cta_policy)
+            _check(load().spa_comm_init_config(ctypes.byref(h), uid, nranks, rank, device, ctypes.byref(cfg)),
+                   "spa_comm_init_config")
+        else:
+            _check(load().spa_comm_init(ctypes.byref(h), uid, nranks, rank, device), "spa_comm_init")
         return cls(h.value)
+
+    def wait(self, stream=None, timeout_ms: int = -1):
+        """Block until `stream` completes; a failed peer or the timeout aborts the NCCL communicator (SpaError)."""
+        _check(load().spa_comm_wait(self.h, _stream(stream), timeout_ms), "spa_comm_wait")
 
     @classmethod
     def loopback(cls, nvirtual: int, device: int = 0) -> "Comm":

@@ -233,3 +233,11 @@ def test_p2p_comm_needs_a_device():
     with pytest.raises(spa.SpaError) as e:
         spa.Comm.p2p(2, 0, 0)
     assert e.value.status == 4
+
+
+@pytest.mark.parametrize("cfg", [dict(min_ctas=-1), dict(min_ctas=8, max_ctas=4), dict(cta_policy=3)])
+def test_nccl_config_validated_before_any_call(cfg):
+    """spa_comm_init_config rejects bad NCCL SM budgets synchronously (SPA_ERR_INVALID), before touching CUDA/NCCL."""
+    with pytest.raises(spa.SpaError) as e:
+        spa.Comm.nccl(b"\0" * 128, 2, 0, 0, **{"min_ctas": 0, "max_ctas": 0, "cta_policy": 0, **cfg})
+    assert e.value.status == 1
