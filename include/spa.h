@@ -318,6 +318,10 @@ spa_status spa_plan_describe_pack(const spa_plan *plan, int rank, spa_copy_desc 
 spa_status spa_plan_describe_unpack(const spa_plan *plan, int rank, spa_copy_desc *out, int max, int *n);
 spa_status spa_plan_describe_messages(const spa_plan *plan, int stage, int dir, int rank, spa_msg *out, int max,
                                       int *n);
+/* Ring plans: the NCCL messages of ring step t (0 <= t < nranks-1) as `rank` issues them: send K, send V to rank+1
+ * (buf 1/2 = the caller's k/v at t = 0, else 4 = its ws receive slot (t-1)&1), receive K, V from rank-1 into ws slot
+ * t&1.  USP plans: the step of the ring sub-plan, peers as global ranks. */
+spa_status spa_plan_describe_ring(const spa_plan *plan, int step, int rank, spa_msg *out, int max, int *n);
 /* Attention problem of stage k on owner rank `rank`: ws byte offsets of Q, K, V, O and Sq, Skv, n_heads. */
 typedef struct {
     long long q_off, k_off, v_off, o_off;

@@ -2041,6 +2041,35 @@ spa_status spa_plan_describe_messages(const spa_plan *plan, int stage, int dir, 
     return SPA_OK;
 }
 
+// Ring step t of `rank` in the order ring_call issues it: send K, send V (the block held: the caller's at t = 0, else
+// receive slot (t-1)&1) to rank+1, receive K, V from rank-1 into slot t&1.  USP plans: the ring sub-plan's step with
+// peers as global ranks (ring of u = rank % U: ranks rho*U + u).
+spa_status spa_plan_describe_ring(const spa_plan *p, int step, int rank, spa_msg *out, int max, int *n) {
+    if (!p || !n || (!out && max > 0)) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (!p->ring) return fail(SPA_ERR_INVALID, "not a ring plan");
+    if (rank < 0 || rank >= p->P) return fail(SPA_ERR_INVALID, "bad rank");
+    *n = 0;
+    if (p->U > 1) {
+        const int U = p->U, u = rank % U;
+        SPA_TRY(spa_plan_describe_ring(p->ring_plan, step, rank / U, out, max, n));
+        for (int i = 0; i < *n; ++i) out[i].peer = out[i].peer * U + u;
+        return SPA_OK;
+    }
+    const int P = p->P;
+    if (step < 0 || step >= std::max(1, P - 1)) return fail(SPA_ERR_INVALID, "bad ring step");
+    if (P == 1) return SPA_OK;
+    if (max < 4) return fail(SPA_ERR_INVALID, "describe: output too small");
+    const long long blk = p->E_loc * 2;
+    const int next = (rank + 1) % P, prev = (rank + P - 1) % P;
+    const int cur = (step - 1) & 1, nxt = step & 1;
+    out[0] = {next, 0, step == 0 ? BUF_K : BUF_WS, step == 0 ? 0 : p->off_kvbuf + (2LL * cur) * blk, blk};
+    out[1] = {next, 0, step == 0 ? BUF_V : BUF_WS, step == 0 ? 0 : p->off_kvbuf + (2LL * cur + 1) * blk, blk};
+    out[2] = {prev, 1, BUF_WS, p->off_kvbuf + (2LL * nxt) * blk, blk};
+    out[3] = {prev, 1, BUF_WS, p->off_kvbuf + (2LL * nxt + 1) * blk, blk};
+    *n = 4;
+    return SPA_OK;
+}
+
 spa_status spa_plan_describe_attention(const spa_plan *p, int stage, int rank, spa_attn_desc *out) {
     if (!p || !out) return fail(SPA_ERR_INVALID, "NULL argument");
     if (p->ring) return fail(SPA_ERR_INVALID, "ring plan: nothing to describe");

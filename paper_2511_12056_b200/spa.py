@@ -135,6 +135,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "spa_plan_describe_unpack": ([_P, i, ctypes.POINTER(CopyDesc), i, ip], i),
         "spa_plan_describe_messages": ([_P, i, i, i, ctypes.POINTER(Msg), i, ip], i),
         "spa_plan_describe_attention": ([_P, i, i, ctypes.POINTER(AttnDesc)], i),
+        "spa_plan_describe_ring": ([_P, i, i, ctypes.POINTER(Msg), i, ip], i),
         "spa_plan_qkv_weight_bytes": ([_P, i, ctypes.POINTER(ctypes.c_size_t)], i),
         "spa_plan_qkv_workspace_bytes": ([_P, ctypes.POINTER(ctypes.c_size_t)], i),
         "spa_plan_pack_qkv_weight": ([_P, i, _P, _P, _P, _P], i),
@@ -375,6 +376,12 @@ class Plan:
         n = ctypes.c_int()
         _check(load().spa_plan_describe_messages(self.h, stage, direction, rank, out, cap, ctypes.byref(n)),
                "describe_messages")
+        return list(out[:n.value])
+
+    def describe_ring(self, step: int, rank: int) -> List[Msg]:
+        out = (Msg * 8)()
+        n = ctypes.c_int()
+        _check(load().spa_plan_describe_ring(self.h, step, rank, out, 8, ctypes.byref(n)), "describe_ring")
         return list(out[:n.value])
 
     def describe_attention(self, stage: int, rank: int) -> AttnDesc:

@@ -241,3 +241,53 @@ def test_nccl_config_validated_before_any_call(cfg):
     with pytest.raises(spa.SpaError) as e:
         spa.Comm.nccl(b"\0" * 128, 2, 0, 0, **{"min_ctas": 0, "max_ctas": 0, "cta_policy": 0, **cfg})
     assert e.value.status == 1
+
+
+def _match(msgs_of, P):
+    """For every ordered pair (p, q): p's sends to q and q's receives from p, in issue order, pair up one to one
+    with equal sizes (NCCL's matching rule) -- returns the pairs."""
+    pairs = []
+    for p in range(P):
+        for q in range(P):
+            sends = [m for m in msgs_of[p] if not m.is_recv and m.peer == q]
+            recvs = [m for m in msgs_of[q] if m.is_recv and m.peer == p]
+            assert len(sends) == len(recvs), (p, q)
+            for s, r in zip(sends, recvs):
+                assert s.bytes == r.bytes
+                pairs.append((p, s, q, r))
+    return pairs
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_ring_messages_match_and_rotate(P):
+    """Ring plans (R21): every step's sends and receives match across ranks, and after step t rank r's receive slot
+    t&1 holds the K/V block of rank (r - t - 1) mod P (simulated on block labels)."""
+    B, S, H, D = 1, P * 32, 3, 64
+    plans = [spa.Plan(spa.Comm.host(P, r), B, S, H, D, ring=True) for r in range(P)]
+    held = {r: {("K", None): r, ("V", None): r} for r in range(P)}   # block label per (buffer, ws offset)
+    for t in range(P - 1):
+        msgs = {r: plans[r].describe_ring(t, r) for r in range(P)}
+        new = {r: dict(held[r]) for r in range(P)}
+        for p, s, q, r in _match(msgs, P):
+            key = ("K", None) if s.buf == spa.BUF_K else ("V", None) if s.buf == spa.BUF_V else ("WS", s.off)
+            new[q][("WS", r.off)] = held[p][key]
+        held = new
+        for r in range(P):
+            k_slot, v_slot = [m.off for m in msgs[r] if m.is_recv]
+            assert held[r][("WS", k_slot)] == held[r][("WS", v_slot)] == (r - t - 1) % P
+
+
+@pytest.mark.parametrize("P,U", [(4, 2), (8, 2), (8, 4)])
+def test_usp_messages_match(P, U):
+    """USP (R21): the ring steps of every Ulysses index u match across the R = P/U ranks of that ring (global peers),
+    and the Ulysses group exchange (a seq->head reshard over U ranks) matches inside every group."""
+    B, S, H, D = 1, P * 16, 4 * U, 64
+    plans = [spa.Plan(spa.Comm.host(P, r), B, S, H, D, ring=True, ulysses=U) for r in range(P)]
+    R = P // U
+    for t in range(max(1, R - 1)):
+        msgs = {r: plans[r].describe_ring(t, r) for r in range(P)}
+        for p, s, q, r in _match(msgs, P):
+            assert p % U == q % U and q == ((p // U + 1) % R) * U + p % U
+    sub = [spa.Plan(spa.Comm.host(U, u), B, U * (S // P), H, D) for u in range(U)]
+    for d in (0, 1):
+        _match({u: sub[u].describe_messages(0, d, u) for u in range(U)}, U)

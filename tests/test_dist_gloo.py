@@ -5,7 +5,7 @@ runs the described pack jobs, exchanges exactly the described per-stage messages
 process through torch.distributed (gloo) point-to-point, applies an identity "attention" to the
 described regions, runs the output exchange and the described unpack (Psi_g).  The output must
 equal the input element for element, for every stage split, for Aco (1 source + 1 co-processor) and
-for head padding (H odd).
+for head padding (H odd), and the ring plan's described K/V rotation (R21).
 """
 import os
 import socket
@@ -86,6 +86,33 @@ def _worker(rank, world, port, cases, result):
                 hostsim.run_copy(d, ws, out)
             ok &= bool(np.array_equal(out, x))
         plan.close()
+    # ring plan (R21): the described K/V messages of every step, exchanged for real over gloo; after step t the
+    # receive slot holds the blocks of rank (rank - t - 1) mod P
+    B, S, H, D = 1, 2 * 32, 3, 64
+    plan = spa.Plan(spa.Comm.host(world, rank), B, S, H, D, ring=True)
+    blk = B * (S // world) * H * D * 2
+    K = np.full(blk, 10 + rank, dtype=np.uint8)
+    V = np.full(blk, 20 + rank, dtype=np.uint8)
+    ws = np.zeros(plan.workspace_bytes, dtype=np.uint8)
+    for t in range(world - 1):
+        msgs = plan.describe_ring(t, rank)
+        reqs, rbufs = [], []
+        for i, m in enumerate(msgs):
+            if m.is_recv:
+                buf = torch.empty(m.bytes, dtype=torch.uint8)
+                reqs.append(dist.irecv(buf, src=m.peer, tag=100 * t + i - 2))
+                rbufs.append((buf, m.off))
+            else:
+                src = K if m.buf == spa.BUF_K else V if m.buf == spa.BUF_V else ws[m.off:m.off + m.bytes]
+                reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(src)), dst=m.peer, tag=100 * t + i))
+        for q in reqs:
+            q.wait()
+        for buf, off in rbufs:
+            ws[off:off + buf.numel()] = buf.numpy()
+        owner = (rank - t - 1) % world
+        k_off, v_off = [m.off for m in msgs if m.is_recv]
+        ok &= bool((ws[k_off:k_off + blk] == 10 + owner).all() and (ws[v_off:v_off + blk] == 20 + owner).all())
+    plan.close()
     result[rank] = int(ok)
     dist.destroy_process_group()
 
