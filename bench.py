@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
     ap.add_argument("--spawn", action="store_true", help="launch through torch.distributed.run even at N=1")
+    ap.add_argument("--qkv", action="store_true",
+                    help="layer from hidden states: fused QKV projection (f3) + PipeSP; FLOPs include the projection")
     ap.add_argument("--north-star", type=int, default=-1,
                     help="720p N_st sweep block: 1 on, 0 off, -1 (default) on when N == 8")
     return ap.parse_args()
@@ -258,17 +260,30 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    def make(workload, n_st):
+    def make(workload, n_st, qkv_mode=False):
         w = synthgen.WORKLOADS[workload]
         Bw = args.batch or w.B
         S_l = w.S // P
+        plan = spa.Plan(comm, Bw, w.S, w.H, w.D, stages=n_st)
+        if qkv_mode:   # hidden states X [B, S_l, C = H*D], the fused weight packed once for the plan
+            C = w.H * w.D
+            x = synthgen.gen_hidden_shard(0, (Bw, w.S, C), rank * S_l, (rank + 1) * S_l, device=dev)
+            wp = plan.pack_qkv_weight(synthgen.gen_qkv_weight(0, C, w.H, w.D, device=dev),
+                                      synthgen.gen_qkv_bias(0, w.H, w.D, device=dev))
+            out = torch.empty((Bw, S_l, w.H, w.D), dtype=torch.bfloat16, device=dev)
+            return plan, ("qkv", C, x, wp), out, plan.qkv_workspace(dev)
         qkv = [synthgen.gen_qkv_shard(0, t, (Bw, w.S, w.H, w.D), rank * S_l, (rank + 1) * S_l, device=dev)
                for t in range(3)]
-        plan = spa.Plan(comm, Bw, w.S, w.H, w.D, stages=n_st)
         return plan, qkv, torch.empty_like(qkv[0]), plan.workspace(dev)
 
     def call(plan, qkv, out, ws):
-        if P == 1:
+        if qkv[0] == "qkv":
+            _, C, x, wp = qkv
+            if P == 1:
+                spa.spa_pipesp_qkv_attention_local(plan, C, [x], wp, [out], ws, stream)
+            else:
+                spa.spa_pipesp_qkv_attention(plan, C, x, wp, out, ws, stream)
+        elif P == 1:
             spa.spa_pipesp_attention_local(plan, [qkv[0]], [qkv[1]], [qkv[2]], [out], ws, stream)
         else:
             spa.spa_pipesp_attention(plan, *qkv, out, ws, stream)
@@ -305,16 +320,24 @@ def run_ours(args):
     peak = peaks["bf16_tflops"]
 
     # ---------------------------------------------------------------- headline
-    plan, qkv, out, ws = make(name, stages)
+    plan, qkv, out, ws = make(name, stages, args.qkv)
     with ClockSampler(local) as clk:
         step_ms, profs = timed(plan, qkv, out, ws, args.steps, args.warmup, True)
     t_max = max_over_ranks(statistics.median(step_ms))
-    flops = attn_flops(B, S, H, D)
+    proj_flops = 2.0 * B * S * (H * D) * 3 * H * D if args.qkv else 0.0
+    flops = attn_flops(B, S, H, D) + proj_flops
     value = flops / (t_max * 1e-3) / 1e12
     attn_ms = [sum(p.attn_ms[k] for k in range(p.n_stages)) for p in profs]
     a2a_in = [sum(p.a2a_in_ms[k] for k in range(p.n_stages)) for p in profs]
     a2a_out = [sum(p.a2a_out_ms[k] for k in range(p.n_stages)) for p in profs]
-    launches = sum(p.attn_launches + p.copy_launches for p in profs)
+    launches = sum(p.attn_launches + p.copy_launches + p.gemm_launches for p in profs)
+    qkv_info = None
+    if args.qkv:
+        proj_ms = statistics.median([p.pack_ms for p in profs])
+        qkv_info = {"projection_ms": proj_ms, "projection_flops_per_rank": proj_flops / P,
+                    "projection_tflops": proj_flops / P / (proj_ms * 1e-3) / 1e12,
+                    "projection_frac_of_peak": proj_flops / P / (proj_ms * 1e-3) / 1e12 / peak,
+                    "kernel": "qkv_gemm_kernel (tcgen05, fused pack)", "C": H * D}
     exposed, t_nocomm = (None, None)
     a2a = None
     if P > 1:
@@ -332,7 +355,9 @@ def run_ours(args):
     # library's host-buffer call (spa_attention_host), which overlaps head group i's attention with group i+1's
     # H2D and group i-1's D2H; N GPUs: H2D, the SP call, D2H in sequence.
     e2e = None
-    if not args.no_e2e and P == 1:
+    if args.qkv:
+        pass   # e2e of the hidden-state layer: not separately measured (the attention-only line carries e2e)
+    elif not args.no_e2e and P == 1:
         hq = [x.cpu().pin_memory() for x in qkv]
         hout = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
         hplan = spa.Plan(comm, B, S, H, D, stages=args.host_groups)
@@ -375,7 +400,7 @@ def run_ours(args):
                "path": "per rank: H2D of the shard, spa_pipesp_attention, D2H (in sequence)"}
 
     # roofline of the dominant kernel (attention): algorithmic FLOPs per launch / measured duration
-    rank_attn_flops = flops / P
+    rank_attn_flops = attn_flops(B, S, H, D) / P
     attn_ms_med = statistics.median(attn_ms)
     achieved = rank_attn_flops / (attn_ms_med * 1e-3) / 1e12
     traffic = None
@@ -430,14 +455,15 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded splitmix64 Irwin-Hall, D0, seed 0)",
-            "config": {"workload": name, "B": B, "S": S, "H": H, "D": D, "P": P, "stages": stages,
+            "config": {"workload": name + ("+qkv" if args.qkv else ""), "B": B, "S": S, "H": H, "D": D, "P": P,
+                       "stages": stages,
                        "stage_split": split,
                        "parallelism": f"ulysses-sp{P} (PipeSP)" if P > 1 else "single",
                        "timing": "median of per-step CUDA events, max over ranks",
                        "l2": "flushed between timed steps (256 MiB memset, untimed); inputs > L2"},
             "exposed_a2a_pct": exposed, "ms_skip_comm": t_nocomm, "a2a": a2a, "overlapped_roofline": overlapped,
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches,
-            "roofline": roofline, "cpu_baseline": cpu, "north_star": north,
+            "roofline": roofline, "cpu_baseline": cpu, "north_star": north, "qkv_projection": qkv_info,
         }
         print(json.dumps(line), flush=True)
     comm.close()

@@ -169,7 +169,13 @@ spa_status spa_plan_destroy(spa_plan *plan);
  *                          plans only for now (the NVLink version needs registered NCCL windows); same bits. */
 /*   SPA_OPT_COMM_SMS  n -> the persistent QKV-projection GEMM (spa_pipesp_qkv_attention*) leaves n SMs free so that
  *                          the communication kernels of the overlapped all-to-alls get SMs at once (0..64; default 0) */
-enum { SPA_OPT_PROFILE = 1, SPA_OPT_SKIP_COMM = 2, SPA_OPT_COPROC_BUSY = 3, SPA_OPT_DIRECT = 4, SPA_OPT_COMM_SMS = 5 };
+/*   SPA_OPT_RANK_ONLY r+1 -> loopback plans: only virtual rank r's launches and the messages it sends or receives
+ *                          run (0 = all ranks) -- one rank's share of the multi-GPU schedule measured on one GPU
+ *                          (wave tails, copy/attention SM contention); the output is then NOT the attention result
+ *   SPA_OPT_LOOPBACK_CE 1 -> loopback exchange messages as copy-engine cudaMemcpyAsync (the P2P transport's staged
+ *                          exchange) instead of the copy kernel (NCCL-like: SMs move the bytes); same result bits */
+enum { SPA_OPT_PROFILE = 1, SPA_OPT_SKIP_COMM = 2, SPA_OPT_COPROC_BUSY = 3, SPA_OPT_DIRECT = 4, SPA_OPT_COMM_SMS = 5,
+       SPA_OPT_RANK_ONLY = 6, SPA_OPT_LOOPBACK_CE = 7 };
 spa_status spa_plan_set_option(spa_plan *plan, int option, int value);
 
 /* Key-padding mask for the following SP calls of this plan (Alg. 1's attention_mask, PAPER.md:85 and :90,

@@ -115,6 +115,10 @@ struct spa_plan {
     // options
     bool profile = false, skip_comm = false, coproc_busy = false, direct = false;
     int comm_sms = 0;   // SMs the persistent QKV GEMM leaves free for communication kernels (SPA_OPT_COMM_SMS)
+    // measurement modes of loopback plans: only this virtual rank's launches and messages (SPA_OPT_RANK_ONLY, -1 =
+    // all ranks); exchange messages as copy-engine cudaMemcpyAsync instead of the copy kernel (SPA_OPT_LOOPBACK_CE)
+    int rank_only = -1;
+    bool loopback_ce = false;
     // runtime resources (lazy)
     std::vector<cudaEvent_t> sync_ev;  // scheduling events (no timing)
     std::vector<cudaEvent_t> prof_ev;  // timing events
@@ -530,8 +534,15 @@ spa_status run_exchange(Exec &x, int k, int dir) {
             for (const Msg &g : per[src]) if (!g.is_recv && g.peer == dst) sends.push_back(&g);
             for (const Msg &g : per[dst]) if (g.is_recv && g.peer == src) recvs.push_back(&g);
             if (sends.size() != recvs.size()) return fail(SPA_ERR_COMM, "loopback: unmatched messages");
+            if (p->rank_only >= 0 && src != p->rank_only && dst != p->rank_only) continue;
             for (size_t i = 0; i < sends.size(); ++i) {
                 if (sends[i]->bytes != recvs[i]->bytes) return fail(SPA_ERR_COMM, "loopback: size mismatch");
+                if (p->loopback_ce) {   // copy engines, as the P2P transport's staged exchange
+                    SPA_CHECK_CUDA(cudaMemcpyAsync(resolve(x, dst, recvs[i]->buf, recvs[i]->off),
+                                                   resolve(x, src, sends[i]->buf, sends[i]->off),
+                                                   (size_t)sends[i]->bytes, cudaMemcpyDeviceToDevice, x.sm));
+                    continue;
+                }
                 CopyJob j{};
                 j.src = resolve(x, src, sends[i]->buf, sends[i]->off);
                 j.dst = resolve(x, dst, recvs[i]->buf, recvs[i]->off);
@@ -540,7 +551,7 @@ spa_status run_exchange(Exec &x, int k, int dir) {
                 jobs.push_back(j);
             }
         }
-    SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sm, &p->copy_launches));
+    if (!jobs.empty()) SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sm, &p->copy_launches));
     return SPA_OK;
 }
 
@@ -552,6 +563,7 @@ spa_status run_attention(Exec &x, int k, cudaStream_t st) {
     const int nr = (p->comm->kind == KIND_LOOPBACK) ? p->P : 1;
     for (int rr = 0; rr < nr; ++rr) {
         const int r = (p->comm->kind == KIND_LOOPBACK) ? rr : p->comm->rank;
+        if (p->rank_only >= 0 && r != p->rank_only) continue;
         const int nreal = real_heads(p, s, r, kh);   // pad heads are not computed
         if (nreal == 0) continue;
         uint8_t *ws = resolve(x, r, BUF_WS, 0);
@@ -580,6 +592,7 @@ spa_status run_qkv_pack(Exec &x, cudaEvent_t *ev_gemm) {
     for (int kh = 0; kh < s.G_h; ++kh) {
         for (int i = 0; i < nr; ++i) {
             const int r = (p->comm->kind == KIND_LOOPBACK) ? i : p->comm->rank;
+            if (p->rank_only >= 0 && r != p->rank_only) continue;
             uint8_t *ws = resolve(x, r, BUF_WS, 0);
             const long long base = idx_send(p, s, r, kh, 0, 0, 0) * 2;
             void *dst[3] = {ws + p->off_sendQ + base, ws + p->off_sendK + base, ws + p->off_sendV + base};
@@ -597,6 +610,7 @@ spa_status run_pack(Exec &x) {
     const int nr = (p->comm->kind == KIND_LOOPBACK) ? p->Psrc : (is_source(p, p->comm->rank) ? 1 : 0);
     for (int i = 0; i < nr; ++i) {
         const int r = (p->comm->kind == KIND_LOOPBACK) ? i : p->comm->rank;
+        if (p->rank_only >= 0 && r != p->rank_only) continue;
         uint8_t *ws = resolve(x, r, BUF_WS, 0);
         if (x.in_tensors & 1) pack_jobs(p, *x.s, r, x.ptr.q[i], p->off_sendQ, ws, jobs);
         if (x.in_tensors & 2) pack_jobs(p, *x.s, r, x.ptr.k[i], p->off_sendK, ws, jobs);
@@ -613,6 +627,7 @@ spa_status run_unpack(Exec &x) {
     const int nr = (p->comm->kind == KIND_LOOPBACK) ? p->Psrc : (is_source(p, p->comm->rank) ? 1 : 0);
     for (int i = 0; i < nr; ++i) {
         const int r = (p->comm->kind == KIND_LOOPBACK) ? i : p->comm->rank;
+        if (p->rank_only >= 0 && r != p->rank_only) continue;
         unpack_jobs(p, *x.s, r, resolve(x, r, BUF_WS, 0), p->off_orecv, x.ptr.out[i], jobs);
     }
     if (jobs.empty()) return SPA_OK;
@@ -654,6 +669,7 @@ spa_status execute_direct(Exec &x) {
     std::vector<CopyJob> jobs;
     const long long offs[3] = {p->off_recvQ, p->off_recvK, p->off_recvV};
     for (int r = 0; r < p->Psrc; ++r) {
+        if (p->rank_only >= 0 && r != p->rank_only) continue;
         const void *xs[3] = {x.ptr.q[r], x.ptr.k[r], x.ptr.v[r]};
         const long long n = p->len[r];
         for (int t = 0; t < 3; ++t)
@@ -689,7 +705,7 @@ spa_status execute_direct(Exec &x) {
                     }
                 }
     }
-    SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sc, &p->copy_launches));
+    if (!jobs.empty()) SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sc, &p->copy_launches));
     pr.end("pack", x.sc);
     // stages alternate between two streams so stage k+1 fills stage k's wave tail (as in execute())
     if (!p->sc_alt) SPA_CHECK_CUDA(cudaStreamCreateWithFlags(&p->sc_alt, cudaStreamNonBlocking));
@@ -703,6 +719,7 @@ spa_status execute_direct(Exec &x) {
         cudaStream_t st = (k & 1) ? p->sc_alt : x.sc;
         pr.begin(an, st);
         for (int r = 0; r < p->P; ++r) {   // owner r
+            if (p->rank_only >= 0 && r != p->rank_only) continue;
             const int nreal = real_heads(p, s, r, kh);
             if (nreal == 0) continue;
             uint8_t *ws = resolve(x, r, BUF_WS, 0);
@@ -1485,6 +1502,15 @@ spa_status spa_plan_set_option(spa_plan *plan, int option, int value) {
         case SPA_OPT_PROFILE: plan->profile = value != 0; break;
         case SPA_OPT_SKIP_COMM: plan->skip_comm = value != 0; break;
         case SPA_OPT_COPROC_BUSY: plan->coproc_busy = value != 0; break;
+        case SPA_OPT_RANK_ONLY:
+            if (plan->comm->kind != KIND_LOOPBACK || value < 0 || value > plan->P)
+                return fail(SPA_ERR_INVALID, "rank-only mode: loopback plans, value = rank + 1 (0 = off)");
+            plan->rank_only = value - 1;
+            break;
+        case SPA_OPT_LOOPBACK_CE:
+            if (plan->comm->kind != KIND_LOOPBACK) return fail(SPA_ERR_INVALID, "loopback plans only");
+            plan->loopback_ce = value != 0;
+            break;
         case SPA_OPT_COMM_SMS:
             if (value < 0 || value > 64) return fail(SPA_ERR_INVALID, "comm SMs must be in [0, 64]");
             plan->comm_sms = value;

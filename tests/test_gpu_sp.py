@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 import torch
 
+import synthgen
 from oracle import sp as osp
 from paper_2511_12056_b200 import spa
 from tests import gpu_util as U
@@ -218,3 +219,28 @@ def test_direct_transport_bit_identical(P, S, H, stages, pad, n_src, masked):
     call(plan, qs, ks, vs, outs, plan.workspace())
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(outs, dim=1).view(torch.int16), single.view(torch.int16))
+
+
+def test_rank_only_measurement_mode():
+    """SPA_OPT_RANK_ONLY (loopback): only virtual rank r's launches run -- 1 attention launch per stage instead of P,
+    one pack and one unpack; SPA_OPT_LOOPBACK_CE moves the messages with copy engines (no copy-kernel launches)
+    and leaves the result bits unchanged."""
+    B, S, H, D, P = 1, 1024, 8, 64, 4
+    q, k, v = (synthgen.gen_qkv_shard(0, t, (B, S, H, D), 0, S, device="cuda") for t in range(3))
+    S_l = S // P
+    shards = [[x[:, i * S_l:(i + 1) * S_l].contiguous() for i in range(P)] for x in (q, k, v)]
+    outs = [torch.empty_like(t) for t in shards[0]]
+    plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=2)
+    ws = plan.workspace()
+    plan.set_option(spa.SPA_OPT_PROFILE, 1)
+    plan.set_option(spa.SPA_OPT_LOOPBACK_CE, 1)
+    spa.spa_pipesp_attention_local(plan, *shards, outs, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(outs, 1).view(torch.int16), spa.attention(q, k, v).view(torch.int16))
+    assert plan.last_profile().copy_launches == 2   # pack + unpack kernels; the exchange ran on copy engines
+    plan.set_option(spa.SPA_OPT_LOOPBACK_CE, 0)
+    plan.set_option(spa.SPA_OPT_RANK_ONLY, 3)
+    spa.spa_pipesp_attention_local(plan, *shards, outs, ws)
+    torch.cuda.synchronize()
+    prof = plan.last_profile()
+    assert prof.attn_launches == 2 and prof.n_stages == 2
