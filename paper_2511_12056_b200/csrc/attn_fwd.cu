@@ -93,13 +93,16 @@ struct Cfg {
     // S -> softmax -> PV chains: three chains of 128-key tiles.  SPA_NG4_D96 builds D=96 with four chains of
     // 96-key tiles (4 x 96 + 96 = 480 TMEM columns, 104 softmax registers); measured 1-3 % slower
     // (profiles/r01_v5_experiments/README.md), so it is not the default.
+#ifndef SPA_NG4_MASK
 #ifdef SPA_NG4_D96
-    static constexpr int BN = (D == 96) ? 96 : 128;
-    static constexpr int NG = (D == 96) ? 4 : 3;
+#define SPA_NG4_MASK 2
 #else
-    static constexpr int BN = 128;
-    static constexpr int NG = 3;
+#define SPA_NG4_MASK 0   // bit 0: D = 64, bit 1: D = 96, bit 2: D = 128 -> four chains of 96-key tiles
 #endif
+#endif
+    static constexpr bool NG4 = ((SPA_NG4_MASK >> (D == 64 ? 0 : (D == 96 ? 1 : 2))) & 1) != 0;
+    static constexpr int BN = NG4 ? 96 : 128;
+    static constexpr int NG = NG4 ? 4 : 3;
     static constexpr int HALF = BN / 2;                  // keys per P release (64 or 48)
     static constexpr int NUM_SOFTMAX_WARPS = 4 * NG;
     // Warpgroup 0 = {producer, 2 idle, MMA issuer}, then NG warpgroups of softmax warps.  Warpgroup 0 gives its
@@ -137,7 +140,7 @@ struct Cfg {
     static constexpr int HALF_BYTES = KV_TILE_BYTES / 2; // one ring slot: this CTA's half of a K or V tile
     static constexpr int KCHUNK = (BN / 2) * 128;        // K half: BN/2 keys; 64-column SW128 chunk c at c*KCHUNK
     // K/V ring slots (as many as fit: the ring depth is the TMA lookahead that hides L2 latency)
-    static constexpr int NS = (D == 128) ? 12 : 16;
+    static constexpr int NS = (D == 128 && BN == 128) ? 12 : 16;
     static constexpr int BAR_BYTES = 512;
     static constexpr int XCH_BYTES = BM * 4;   // static smem: running max (the epilogue's (m, l) reuse ring slot 0)
     static constexpr int SMEM_BYTES = 1024 /*align slack*/ + TILE_BYTES + NS * HALF_BYTES + BAR_BYTES;

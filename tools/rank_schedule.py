@@ -75,6 +75,14 @@ def main():
             ws = plan.qkv_workspace() if args.qkv else plan.workspace()
             wp = plan.pack_qkv_weight(W, bias) if args.qkv else None
             nbytes = sent_bytes(plan, r)
+            # one full call (all virtual ranks) first: every buffer the rank-only calls read then holds real data --
+            # the attention's power draw, and so the power-capped clock, depends on the operand values
+            plan.set_option(spa.SPA_OPT_RANK_ONLY, 0)
+            if args.qkv:
+                spa.spa_pipesp_qkv_attention_local(plan, C, xs, wp, outs, ws)
+            else:
+                spa.spa_pipesp_attention_local(plan, *shards, outs, ws)
+            torch.cuda.synchronize()
             res = {}
             for mode in args.modes.split(","):
                 if args.qkv and mode == "direct":
