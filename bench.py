@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
     ap.add_argument("--spawn", action="store_true", help="launch through torch.distributed.run even at N=1")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1 exchange: NCCL grouped send/recv, or CUDA IPC peer memory with copy engines (f1)")
+    ap.add_argument("--direct", action="store_true", help="p2p transport: pack / epilogue store to peers (f1)")
     ap.add_argument("--qkv", action="store_true",
                     help="layer from hidden states: fused QKV projection (f3) + PipeSP; FLOPs include the projection")
     ap.add_argument("--north-star", type=int, default=-1,
@@ -229,10 +232,20 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # SPA_BENCH_SHARED_GPU=1: every rank on cuda:0 with a gloo process group -- exercises the N-rank p2p plumbing
+    # (spawn, CUDA IPC set-up, cross-process flags) on a one-GPU box; its timings mean nothing
+    shared = os.environ.get("SPA_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
+        if world > 1 and args.transport != "p2p":
+            raise SystemExit("SPA_BENCH_SHARED_GPU needs --transport p2p (NCCL refuses two ranks on one GPU)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     name, B, S, H, D = workload_cfg(args)
     P = world
     if S % P or H % P:
@@ -243,6 +256,8 @@ def run_ours(args):
 
     if P == 1:
         comm = spa.Comm.loopback(1, local)
+    elif args.transport == "p2p":
+        comm = spa.Comm.p2p(P, rank, local)
     else:
         obj = [spa.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -255,7 +270,7 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        t = torch.tensor([float(x)], device=dev)
+        t = torch.tensor([float(x)], device="cpu" if shared else dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
@@ -271,10 +286,17 @@ def run_ours(args):
             wp = plan.pack_qkv_weight(synthgen.gen_qkv_weight(0, C, w.H, w.D, device=dev),
                                       synthgen.gen_qkv_bias(0, w.H, w.D, device=dev))
             out = torch.empty((Bw, S_l, w.H, w.D), dtype=torch.bfloat16, device=dev)
-            return plan, ("qkv", C, x, wp), out, plan.qkv_workspace(dev)
+            return plan, ("qkv", C, x, wp), out, p2p_setup(plan, plan.qkv_workspace(dev))
         qkv = [synthgen.gen_qkv_shard(0, t, (Bw, w.S, w.H, w.D), rank * S_l, (rank + 1) * S_l, device=dev)
                for t in range(3)]
-        return plan, qkv, torch.empty_like(qkv[0]), plan.workspace(dev)
+        return plan, qkv, torch.empty_like(qkv[0]), p2p_setup(plan, plan.workspace(dev))
+
+    def p2p_setup(plan, ws):
+        if P > 1 and args.transport == "p2p":   # map every rank's workspace (CUDA IPC handles over torch.distributed)
+            plan.ipc_setup(ws)
+            if args.direct:
+                plan.set_option(spa.SPA_OPT_DIRECT, 1)
+        return ws
 
     def call(plan, qkv, out, ws):
         if qkv[0] == "qkv":
@@ -459,6 +481,7 @@ def run_ours(args):
                        "stages": stages,
                        "stage_split": split,
                        "parallelism": f"ulysses-sp{P} (PipeSP)" if P > 1 else "single",
+                       "transport": (args.transport + ("-direct" if args.direct else "")) if P > 1 else None,
                        "timing": "median of per-step CUDA events, max over ranks",
                        "l2": "flushed between timed steps (256 MiB memset, untimed); inputs > L2"},
             "exposed_a2a_pct": exposed, "ms_skip_comm": t_nocomm, "a2a": a2a, "overlapped_roofline": overlapped,
