@@ -58,6 +58,7 @@ def _check_projection(X, W, b, outs, H, D, rows=None):
     (2, 300, 200, 4, 96),     # ragged M (600 rows), N = 1152 (4.5 tiles), K tail (200 = 3*64 + 8)
     (1, 1000, 512, 2, 128),   # ragged M, N = 768
     (1, 4104, 384, 8, 128),   # many tiles: persistent loop over > 1 tile per pair
+    (1, 100, 64, 1, 64),      # M < one CTA tile, N = 192 < one pair tile, K = one step
 ])
 def test_projection_vs_oracle(B, S, C, H, D):
     X, W, b = _inputs(B, S, C, H, D)
