@@ -302,6 +302,16 @@ spa_status spa_attention_fwd_masked(const void *q, const void *k, const void *v,
                                     long long kv_tok_stride, long long kv_batch_stride, long long o_tok_stride,
                                     long long o_batch_stride, const int32_t *kv_len, void *stream);
 
+/* The same kernel with the diagnostic outputs of SURVEY §8(c) c11: out_fp32 = 1 writes o as fp32 (the normalised
+ * fp32 accumulator, element strides unchanged; bf16(o_fp32) equals the bf16 output bit for bit), and lse (NULL or
+ * fp32 [B][Sq][n_heads]) receives each row's log-sum-exp ln sum_t exp(q.k_t / sqrt(D)) over its valid keys (-inf
+ * when none) -- what partial results over disjoint key blocks are merged with (R21). */
+spa_status spa_attention_fwd_ex(const void *q, const void *k, const void *v, void *o, int B, int Sq, int Skv,
+                                int n_heads, int D, long long q_tok_stride, long long q_batch_stride,
+                                long long kv_tok_stride, long long kv_batch_stride, long long o_tok_stride,
+                                long long o_batch_stride, const int32_t *kv_len, int out_fp32, float *lse,
+                                void *stream);
+
 /* ------------------------------------------------------------------ host-side description (no GPU needed)
  * Buffers: 0 q, 1 k, 2 v, 3 out (the caller's, of source rank `src`), 4 ws (of rank `rank`). */
 typedef struct {

@@ -2007,6 +2007,31 @@ spa_status spa_attention_fwd_masked(const void *q, const void *k, const void *v,
     return SPA_OK;
 }
 
+spa_status spa_attention_fwd_ex(const void *q, const void *k, const void *v, void *o, int B, int Sq, int Skv,
+                                int n_heads, int D, long long q_tok_stride, long long q_batch_stride,
+                                long long kv_tok_stride, long long kv_batch_stride, long long o_tok_stride,
+                                long long o_batch_stride, const int32_t *kv_len, int out_fp32, float *lse,
+                                void *stream) {
+    SPA_TRY(check_ptr(q, "q")); SPA_TRY(check_ptr(k, "k")); SPA_TRY(check_ptr(v, "v")); SPA_TRY(check_ptr(o, "o"));
+    if (D != 64 && D != 96 && D != 128) return fail(SPA_ERR_UNSUPPORTED, "D must be 64, 96 or 128");
+    if (B < 1 || Sq < 1 || Skv < 1 || n_heads < 1) return fail(SPA_ERR_SHAPE, "B, Sq, Skv, n_heads must be >= 1");
+    if (out_fp32 != 0 && out_fp32 != 1) return fail(SPA_ERR_INVALID, "out_fp32 must be 0 or 1");
+    for (long long st : {q_tok_stride, q_batch_stride, kv_tok_stride, kv_batch_stride, o_tok_stride, o_batch_stride})
+        if (st % 8) return fail(SPA_ERR_INVALID, "strides must be multiples of 8 elements (16 bytes)");
+    if (q_tok_stride < (long long)n_heads * D || kv_tok_stride < (long long)n_heads * D ||
+        o_tok_stride < (long long)n_heads * D)
+        return fail(SPA_ERR_SHAPE, "token stride smaller than n_heads*D");
+    if (kv_len && reinterpret_cast<uintptr_t>(kv_len) % 4) return fail(SPA_ERR_INVALID, "kv_len not 4-byte aligned");
+    if (lse && reinterpret_cast<uintptr_t>(lse) % 4) return fail(SPA_ERR_INVALID, "lse not 4-byte aligned");
+    AttnProblem a{q, k, v, out_fp32 ? nullptr : o, B, Sq, Skv, n_heads, D, q_tok_stride, q_batch_stride,
+                  kv_tok_stride, kv_batch_stride, o_tok_stride, o_batch_stride, kv_len};
+    if (out_fp32) a.o32 = o;
+    a.lse = lse;
+    cudaError_t e = launch_attention(a, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return fail(SPA_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
+    return SPA_OK;
+}
+
 spa_status spa_attention_fwd(const void *q, const void *k, const void *v, void *o, int B, int Sq, int Skv,
                              int n_heads, int D, long long q_tok_stride, long long q_batch_stride,
                              long long kv_tok_stride, long long kv_batch_stride, long long o_tok_stride,

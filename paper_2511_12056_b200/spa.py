@@ -15,7 +15,7 @@ from . import _build
 
 __all__ = [
     "SpaError", "load", "header_functions", "get_unique_id", "Comm", "Plan", "Shape", "Profile",
-    "spa_attention_fwd", "spa_attention_fwd_masked", "spa_pipesp_attention", "spa_ulysses_attention", "spa_aco_attention",
+    "spa_attention_fwd", "spa_attention_fwd_masked", "spa_attention_fwd_ex", "attention_fp32", "spa_pipesp_attention", "spa_ulysses_attention", "spa_aco_attention",
     "spa_pipesp_attention_local", "spa_ulysses_attention_local", "spa_aco_attention_local",
     "spa_ring_attention", "spa_ring_attention_local", "spa_attention_host",
     "spa_reshard_seq_to_head", "spa_reshard_head_to_seq", "spa_reshard_seq_to_head_local",
@@ -133,6 +133,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "spa_reshard_head_to_seq_local": ([_P, _PP, _PP, _P, _P], i),
         "spa_attention_fwd": ([_P, _P, _P, _P, i, i, i, i, i, _LL, _LL, _LL, _LL, _LL, _LL, _P], i),
         "spa_attention_fwd_masked": ([_P, _P, _P, _P, i, i, i, i, i, _LL, _LL, _LL, _LL, _LL, _LL, _P, _P], i),
+        "spa_attention_fwd_ex": ([_P, _P, _P, _P, i, i, i, i, i, _LL, _LL, _LL, _LL, _LL, _LL, _P, i, _P, _P], i),
         "spa_plan_describe_pack": ([_P, i, ctypes.POINTER(CopyDesc), i, ip], i),
         "spa_plan_describe_unpack": ([_P, i, ctypes.POINTER(CopyDesc), i, ip], i),
         "spa_plan_describe_messages": ([_P, i, i, i, ctypes.POINTER(Msg), i, ip], i),
@@ -411,6 +412,25 @@ def spa_attention_fwd_masked(q, k, v, o, B, Sq, Skv, n_heads, D, q_tok_stride, q
                                            q_tok_stride, q_batch_stride, kv_tok_stride, kv_batch_stride,
                                            o_tok_stride, o_batch_stride, _ptr(kv_len), _stream(stream)),
            "spa_attention_fwd_masked")
+
+
+def spa_attention_fwd_ex(q, k, v, o, B, Sq, Skv, n_heads, D, q_tok_stride, q_batch_stride, kv_tok_stride,
+                         kv_batch_stride, o_tok_stride, o_batch_stride, kv_len=None, out_fp32=0, lse=None, stream=None):
+    _check(load().spa_attention_fwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(o), B, Sq, Skv, n_heads, D, q_tok_stride,
+                                       q_batch_stride, kv_tok_stride, kv_batch_stride, o_tok_stride, o_batch_stride,
+                                       _ptr(kv_len), int(out_fp32), _ptr(lse), _stream(stream)), "spa_attention_fwd_ex")
+
+
+def attention_fp32(q, k, v, kv_len=None, stream=None):
+    """Diagnostic single-GPU attention on contiguous bf16 [B, S, H, D]: (fp32 output [B, S, H, D], lse [B, S, H])."""
+    import torch
+    B, Sq, H, D = q.shape
+    Skv = k.shape[1]
+    o = torch.empty((B, Sq, H, D), dtype=torch.float32, device=q.device)
+    lse = torch.empty((B, Sq, H), dtype=torch.float32, device=q.device)
+    spa_attention_fwd_ex(q, k, v, o, B, Sq, Skv, H, D, H * D, Sq * H * D, H * D, Skv * H * D, H * D, Sq * H * D,
+                         kv_len, 1, lse, stream)
+    return o, lse
 
 
 def attention(q, k, v, out=None, stream=None, kv_len=None):

@@ -114,3 +114,22 @@ def test_attention_from_host_buffers(stages):
     spa.spa_attention_host(plan, hq, hk, hv, ho, ws)
     torch.cuda.synchronize()
     assert torch.equal(ho.view(torch.int16), ref.cpu().view(torch.int16))
+
+
+@pytest.mark.parametrize("S,D", [(300, 64), (1000, 96), (2048, 128)])
+def test_fp32_output_and_lse_diagnostics(S, D):
+    """spa_attention_fwd_ex: the fp32 output rounds to exactly the bf16 output, is within the
+    tolerance of the fp64 oracle (closer than bf16), and the per-row lse matches the oracle's log-sum-exp."""
+    import oracle
+    B, H = 1, 3
+    q, k, v = U.qkv(B, S, H, D, seed=5)
+    o16 = spa.attention(q, k, v)
+    o32, lse = spa.attention_fp32(q, k, v)
+    torch.cuda.synchronize()
+    assert torch.equal(o32.to(torch.bfloat16).view(torch.int16), o16.view(torch.int16))
+    for h in range(H):
+        ref, ref_lse = oracle.attention_rows_lse(q[0, :, h].double().cpu().numpy(), k[0, :, h].double().cpu().numpy(),
+                                                 v[0, :, h].double().cpu().numpy())
+        ma, rl = U.errors(o32[0, :, h], ref)
+        assert ma <= U.MAX_ABS and rl <= U.REL_L2
+        assert abs(lse[0, :, h].double().cpu().numpy() - ref_lse).max() < 1e-3
