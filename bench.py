@@ -314,6 +314,8 @@ def run_ours(args):
         """Per-step CUDA-event times (ms) on the calling stream, L2 flushed (untimed) before every step."""
         for _ in range(warm):
             call(plan, qkv, out, ws)
+            if P > 1:   # a stuck exchange aborts the communicator and fails the run instead of hanging it
+                comm.wait(stream, timeout_ms=300_000)
         barrier()
         plan.set_option(spa.SPA_OPT_PROFILE, int(profile))
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
