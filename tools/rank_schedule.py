@@ -45,6 +45,8 @@ def main():
     ap.add_argument("--modes", default="skip,kernel,ce,direct")
     ap.add_argument("--reps", type=int, default=7)
     ap.add_argument("--qkv", action="store_true", help="layer from hidden states (fused QKV projection, f3)")
+    ap.add_argument("--aco", type=int, default=0,
+                    help="Aco plan: n_src source ranks of P (PAPER.md:150-199); --rank may name a co-processor")
     ap.add_argument("--peak", type=float, default=None, help="bf16 TF/s (default MEASURED_PEAKS.json)")
     args = ap.parse_args()
     peak = args.peak
@@ -58,30 +60,37 @@ def main():
     for name in args.workloads.split(","):
         w = synthgen.WORKLOADS[name]
         B, S, H, D = w.B, w.S, w.H, w.D
-        S_l = S // P
+        nsrc = args.aco or P
+        bnd = [0]   # source shards differ by <= 1 token (R9)
+        for q in range(nsrc):
+            bnd.append(bnd[-1] + S // nsrc + (1 if q < S % nsrc else 0))
+        S_l = S // nsrc
         C = H * D
         if args.qkv:
-            xs = [synthgen.gen_hidden_shard(0, (B, S, C), q * S_l, (q + 1) * S_l, device="cuda") for q in range(P)]
+            xs = [synthgen.gen_hidden_shard(0, (B, S, C), bnd[q], bnd[q + 1], device="cuda") for q in range(P)]
             W = synthgen.gen_qkv_weight(0, C, H, D, device="cuda")
             bias = synthgen.gen_qkv_bias(0, H, D, device="cuda")
         else:
-            shards = [[synthgen.gen_qkv_shard(0, t, (B, S, H, D), q * S_l, (q + 1) * S_l, device="cuda")
-                       for q in range(P)] for t in range(3)]
-        outs = [torch.empty((B, S_l, H, D), dtype=torch.bfloat16, device="cuda") for _ in range(P)]
+            shards = [[synthgen.gen_qkv_shard(0, t, (B, S, H, D), bnd[q], bnd[q + 1], device="cuda")
+                       for q in range(nsrc)] for t in range(3)]
+        outs = [torch.empty((B, bnd[q + 1] - bnd[q], H, D), dtype=torch.bfloat16, device="cuda") for q in range(nsrc)]
         attn_flops_rank = 4.0 * B * S * S * H * D / P
         proj_flops_rank = 2.0 * B * S_l * C * 3 * H * D if args.qkv else 0.0
+        if args.qkv and args.aco:
+            raise SystemExit("--qkv plans have no co-processor ranks")
         for st in [int(x) for x in args.stages.split(",")]:
-            plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=st)
+            plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=st, n_src=args.aco)
             ws = plan.qkv_workspace() if args.qkv else plan.workspace()
             wp = plan.pack_qkv_weight(W, bias) if args.qkv else None
             nbytes = sent_bytes(plan, r)
             # one full call (all virtual ranks) first: every buffer the rank-only calls read then holds real data --
             # the attention's power draw, and so the power-capped clock, depends on the operand values
             plan.set_option(spa.SPA_OPT_RANK_ONLY, 0)
+            sp_call = spa.spa_aco_attention_local if args.aco else spa.spa_pipesp_attention_local
             if args.qkv:
                 spa.spa_pipesp_qkv_attention_local(plan, C, xs, wp, outs, ws)
             else:
-                spa.spa_pipesp_attention_local(plan, *shards, outs, ws)
+                sp_call(plan, *shards, outs, ws)
             torch.cuda.synchronize()
             res = {}
             for mode in args.modes.split(","):
@@ -96,7 +105,7 @@ def main():
                     if args.qkv:
                         spa.spa_pipesp_qkv_attention_local(plan, C, xs, wp, outs, ws)
                     else:
-                        spa.spa_pipesp_attention_local(plan, *shards, outs, ws)
+                        sp_call(plan, *shards, outs, ws)
                 for _ in range(2):
                     call()
                 torch.cuda.synchronize()
@@ -116,7 +125,7 @@ def main():
                 pm = prof[len(prof) // 2]
                 res[mode] = ms
                 t_roof = max((attn_flops_rank + proj_flops_rank) / (peak * 1e12), nbytes / 900e9) * 1e3
-                rec = {"workload": name, "P": P, "rank": r, "stages": st, "stage_split": list(plan.stage_split),
+                rec = {"workload": name, "P": P, "n_src": nsrc, "rank": r, "stages": st, "stage_split": list(plan.stage_split),
                        "mode": mode, "qkv": args.qkv, "ms_per_layer": ms,
                        "tflops_per_gpu": (attn_flops_rank + proj_flops_rank) / (ms * 1e-3) / 1e12,
                        "tflops_aggregate_if_P_gpus": P * (attn_flops_rank + proj_flops_rank) / (ms * 1e-3) / 1e12,
