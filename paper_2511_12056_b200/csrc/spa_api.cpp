@@ -13,6 +13,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
+#include <nvtx3/nvToolsExtCudaRt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -57,6 +59,15 @@ enum Kind { KIND_NCCL = 0, KIND_LOOPBACK = 1, KIND_HOST = 2, KIND_P2P = 3 };
 enum Buf { BUF_Q = 0, BUF_K = 1, BUF_V = 2, BUF_OUT = 3, BUF_WS = 4, BUF_XHEAD = 5 };
 
 long long align_up(long long x, long long a) { return (x + a - 1) / a * a; }
+
+// NVTX range around the host-side enqueue of a call / step (tracing): visible in Nsight Systems next to
+// the kernels and copies it issues; free when no tool is attached (NVTX3 is header-only, loaded on demand).
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 }  // namespace
 
@@ -308,6 +319,7 @@ spa_status ensure_stream(spa_comm *c) {
     int lo = 0, hi = 0;
     SPA_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     SPA_CHECK_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi));
+    nvtxNameCudaStreamA(c->stream, "spa comm stream");
     return SPA_OK;
 }
 
@@ -659,6 +671,7 @@ void finish_profile(spa_plan *p, const Prof &pr, int n_stages) {
 // exchange fused: no orecv, no unpack).  On NVLink the same jobs / row tables use peer pointers of registered
 // NCCL windows plus a per-stage barrier; on one GPU the "peers" are the virtual ranks' local buffers.
 spa_status execute_direct(Exec &x) {
+    NvtxRange range("spa: direct transport (loopback)");
     spa_plan *p = x.p;
     const Split &s = *x.s;
     const int N = s.n();
@@ -761,6 +774,7 @@ spa_status execute_direct(Exec &x) {
 // landing buffer to `out` once every owner signalled.  Same jobs / row tables as the loopback model above, with the
 // peers' workspaces instead of local ones, and epoch flags instead of stream order.
 spa_status execute_direct_p2p(Exec &x) {
+    NvtxRange range("spa: direct transport (p2p)");
     spa_plan *p = x.p;
     const Split &s = *x.s;
     const int N = s.n(), me = p->comm->rank;
@@ -871,6 +885,7 @@ spa_status execute_direct_p2p(Exec &x) {
 
 // The whole call: single-rank fast path, else the staged pipeline.
 spa_status execute(Exec &x) {
+    NvtxRange range(x.qkv ? "spa: qkv + sp attention" : (x.has_attn ? "spa: sp attention" : "spa: reshard"));
     spa_plan *p = x.p;
     p->attn_launches = 0;
     p->copy_launches = 0;
@@ -945,6 +960,7 @@ spa_status execute(Exec &x) {
     if (!x.qkv) SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_pack, 0));
 
     auto issue_in = [&](int k) -> spa_status {
+        NvtxRange r_in("spa: input exchange");
         if (x.qkv && k % s.C == 0) SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_gemm[k / s.C], 0));
         const std::string nm = "in" + std::to_string(k);
         pr.begin(nm, x.sm);
@@ -958,6 +974,7 @@ spa_status execute(Exec &x) {
         if (N > 1) SPA_TRY(issue_in(1));
         for (int k = 0; k < N; ++k) {
             cudaStream_t st = (k & 1) ? x.sc_alt : x.sc;
+            NvtxRange r_stage("spa: stage");
             SPA_CHECK_CUDA(cudaStreamWaitEvent(st, ev_in[k], 0));
             if (p2p && !p->skip_comm) SPA_TRY(p2p_wait(p, st, FLAG_IN, k));   // the peers' pieces of stage k
             const std::string an = "attn" + std::to_string(k);
@@ -1748,6 +1765,7 @@ static AttnProblem ring_problem(const spa_plan *p, const void *q, const void *k,
 static spa_status ring_call(spa_plan *p, int n, const void *const q[], const void *const k[], const void *const v[],
                             void *const out[], void *ws, void *stream, bool local) {
     if (!p) return fail(SPA_ERR_INVALID, "plan is NULL");
+    NvtxRange range("spa: ring attention");
     if (!p->ring) return fail(SPA_ERR_INVALID, "not a ring plan (shape.ring = 1)");
     if (p->U > 1) {
         // the ring runs over the Ulysses groups, whose token blocks are contiguous in the global sequence
@@ -1903,6 +1921,7 @@ spa_status spa_plan_host_workspace_bytes(const spa_plan *plan, size_t *bytes) {
 spa_status spa_attention_host(spa_plan *p, const void *q, const void *k, const void *v, void *o, void *ws,
                               void *stream) {
     if (!p || !q || !k || !v || !o || !ws) return fail(SPA_ERR_INVALID, "NULL argument");
+    NvtxRange range("spa: attention from host buffers");
     if (p->P != 1 || p->ring || p->comm->kind != KIND_LOOPBACK)
         return fail(SPA_ERR_INVALID, "host-buffer calls need a 1-rank loopback plan");
     SPA_TRY(check_ptr(ws, "ws"));
