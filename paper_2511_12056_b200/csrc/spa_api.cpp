@@ -478,6 +478,20 @@ spa_status p2p_wait(spa_plan *p, cudaStream_t st, int kind, int k) {
     }
     return SPA_OK;
 }
+// single-peer forms (the ring): this rank's flag `kind/k` in rank dst's block; wait for src's flag in this rank's block
+spa_status p2p_signal_one(spa_plan *p, cudaStream_t st, int kind, int k, int dst) {
+    CUdeviceptr a = reinterpret_cast<CUdeviceptr>(p->peer_ws[dst] + p->off_flags) + 4 * flag_slot(p, kind, k, p->comm->rank);
+    if (drv().write32(reinterpret_cast<CUstream>(st), a, p->epoch, 0) != CUDA_SUCCESS)
+        return fail(SPA_ERR_CUDA, "cuStreamWriteValue32 to a peer flag failed");
+    return SPA_OK;
+}
+spa_status p2p_wait_one(spa_plan *p, cudaStream_t st, int kind, int k, int src) {
+    CUdeviceptr a = reinterpret_cast<CUdeviceptr>(p->peer_ws[p->comm->rank] + p->off_flags) + 4 * flag_slot(p, kind, k, src);
+    if (drv().wait32(reinterpret_cast<CUstream>(st), a, p->epoch,
+                     CU_STREAM_WAIT_VALUE_GEQ | (p->p2p_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0)) != CUDA_SUCCESS)
+        return fail(SPA_ERR_CUDA, "cuStreamWaitValue32 on a flag failed");
+    return SPA_OK;
+}
 // every rank has finished its previous call (its buffers may be written): a cross-process barrier on `st`
 spa_status p2p_barrier(spa_plan *p, cudaStream_t st) {
     SPA_TRY(p2p_signal(p, st, FLAG_READY, 0));
@@ -1414,7 +1428,8 @@ spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *sha
     if (s.ulysses < 0 || (!s.ring && s.ulysses > 1)) return fail(SPA_ERR_INVALID, "ulysses degree needs ring = 1");
     if (s.ring && (s.stages != 1 || s.pad_heads != 0))
         return fail(SPA_ERR_INVALID, "ring / USP plans take stages = 1 and pad_heads = 0");
-    if (s.ring && comm->kind == KIND_P2P) return fail(SPA_ERR_UNSUPPORTED, "ring / USP plans need an NCCL or loopback comm");
+    if (s.ring && s.ulysses > 1 && comm->kind == KIND_P2P)
+        return fail(SPA_ERR_UNSUPPORTED, "USP plans need an NCCL or loopback comm");
     if (s.ring && s.ulysses > 1) return create_usp_plan(plan, comm, s);
     if (s.ring) {
         // Ring attention: every rank keeps all heads; only S % P matters.
@@ -1431,6 +1446,10 @@ spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *sha
             p->off_kvbuf = take(4 * p->E_loc * 2);                        // [slot 0/1][K/V] bf16
             p->off_parts = take((long long)P * p->E_loc * 4);             // [P] fp32 partial O
             p->off_lse = take((long long)P * (p->E_loc / s.D) * 4);       // [P] fp32 lse
+            if (comm->kind == KIND_P2P) {   // ring steps' arrival / slot-free flags
+                p->n_flag_stages = P;
+                p->off_flags = take(flag_bytes(p));
+            }
         }
         p->ws_rank_bytes = off;
         *plan = p;
@@ -1823,6 +1842,65 @@ static spa_status ring_call(spa_plan *p, int n, const void *const q[], const voi
         pr.begin("unpack", sc);   // the lse merge
         for (int r = 0; r < P; ++r) SPA_TRY(merge(r, out[r]));
         pr.end("unpack", sc);
+        pr.end("total", sc);
+        finish_profile(p, pr, P);
+        return SPA_OK;
+    }
+    if (p->comm->kind == KIND_P2P) {
+        // P2P ring (CUDA IPC): comm step t copies (copy engines) the block this rank holds -- its own K/V at t = 0, the
+        // block received at step t-1 afterwards -- into rank r+1's receive slot t&1 and raises r+1's arrival flag t;
+        // attention step t >= 1 waits for the arrival flag t-1 from rank r-1.  A slot is reused two steps later, so
+        // comm step t >= 2 into rank r+1 waits for r+1's "slot free" flag t, raised once r+1's attention step t-1 and
+        // its own forwarding copy of that block (comm step t-1) are done.
+        SPA_TRY(ensure_stream(p->comm));
+        cudaStream_t sm = p->comm->stream;
+        cudaEvent_t *ev = p->sync_ev.data();
+        cudaEvent_t ev_entry = ev[0], ev_done = ev[1];
+        cudaEvent_t *comp = ev + 4, *cev = ev + 4 + P;
+        const int r = p->comm->rank, next = (r + 1) % P, prev = (r + P - 1) % P;
+        const size_t blk = (size_t)p->E_loc * 2;
+        auto slotK = [&](int rank, int s) { return resolve(x, rank, BUF_WS, p->off_kvbuf + (long long)(2 * s) * blk); };
+        auto slotV = [&](int rank, int s) { return resolve(x, rank, BUF_WS, p->off_kvbuf + (long long)(2 * s + 1) * blk); };
+        const bool comm_on = !p->skip_comm;
+        ++p->epoch;
+        SPA_CHECK_CUDA(cudaEventRecord(ev_entry, sc));
+        SPA_CHECK_CUDA(cudaStreamWaitEvent(sm, ev_entry, 0));
+        SPA_TRY(p2p_barrier(p, sm));   // every rank finished its previous call: its slots may be written
+        for (int t = 0; t < P; ++t) {
+            const void *ck = t == 0 ? k[0] : slotK(r, (t - 1) & 1);
+            const void *cv = t == 0 ? v[0] : slotV(r, (t - 1) & 1);
+            if (t + 1 < P) {
+                const std::string cn = "in" + std::to_string(t);
+                pr.begin(cn, sm);
+                if (comm_on) {
+                    if (t >= 1) SPA_TRY(p2p_wait_one(p, sm, FLAG_IN, t - 1, prev));   // the block to forward arrived
+                    if (t >= 2) SPA_TRY(p2p_wait_one(p, sm, FLAG_OUT, t, next));      // next's slot t&1 is free
+                    SPA_CHECK_CUDA(cudaMemcpyAsync(slotK(next, t & 1), ck, blk, cudaMemcpyDeviceToDevice, sm));
+                    SPA_CHECK_CUDA(cudaMemcpyAsync(slotV(next, t & 1), cv, blk, cudaMemcpyDeviceToDevice, sm));
+                    SPA_TRY(p2p_signal_one(p, sm, FLAG_IN, t, next));
+                }
+                pr.end(cn, sm);
+                SPA_CHECK_CUDA(cudaEventRecord(cev[t], sm));
+            }
+            if (t >= 1 && comm_on) SPA_TRY(p2p_wait_one(p, sc, FLAG_IN, t - 1, prev));   // block of step t arrived
+            AttnProblem a = ring_problem(p, q[0], ck, cv, parts(r) + t * p->E_loc, lses(r) + t * rows, (r - t + P) % P);
+            const std::string an = "attn" + std::to_string(t);
+            pr.begin(an, sc);
+            SPA_CHECK_CUDA(launch_attention(a, sc));
+            pr.end(an, sc);
+            ++p->attn_launches;
+            SPA_CHECK_CUDA(cudaEventRecord(comp[t], sc));
+            // slot (t-1)&1 is free for prev's comm step t+1 once attention t and the forwarding copy t are done
+            if (t >= 1 && t + 1 <= P - 2 && comm_on) {
+                SPA_CHECK_CUDA(cudaStreamWaitEvent(sc, cev[t], 0));
+                SPA_TRY(p2p_signal_one(p, sc, FLAG_OUT, t + 1, prev));
+            }
+        }
+        pr.begin("unpack", sc);   // the lse merge
+        SPA_TRY(merge(r, out[0]));
+        pr.end("unpack", sc);
+        SPA_CHECK_CUDA(cudaEventRecord(ev_done, sm));
+        SPA_CHECK_CUDA(cudaStreamWaitEvent(sc, ev_done, 0));
         pr.end("total", sc);
         finish_profile(p, pr, P);
         return SPA_OK;

@@ -26,8 +26,9 @@ def run(rank: int, world: int, port: int, case: dict, errq):
         for r in range(n_src):
             bounds.append(bounds[-1] + S // n_src + (1 if r < S % n_src else 0))
         src = rank < n_src
+        ring = case.get("ring", False)
         plan = spa.Plan(spa.Comm.p2p(world, rank, 0), B, S, H, D, stages=case.get("stages", 1),
-                        n_src=case.get("n_src", 0))
+                        n_src=case.get("n_src", 0), ring=ring)
         if case.get("direct"):
             plan.set_option(spa.SPA_OPT_DIRECT, 1)
         ws = plan.workspace()
@@ -46,7 +47,14 @@ def run(rank: int, world: int, port: int, case: dict, errq):
         else:
             full = [synthgen.gen_qkv_shard(case.get("seed", 0), t, (B, S, H, D), 0, S, device="cuda")
                     for t in range(3)]
-        ref = spa.attention(*full)
+        if ring:   # the ring's reference bits: the same plan over `world` virtual ranks on one GPU (R21)
+            lp = spa.Plan(spa.Comm.loopback(world), B, S, H, D, ring=True)
+            parts = [[x[:, bounds[r]:bounds[r + 1]].contiguous() for r in range(world)] for x in full]
+            louts = [torch.empty_like(t) for t in parts[0]]
+            spa.spa_ring_attention_local(lp, *parts, louts, lp.workspace())
+            ref = torch.cat(louts, dim=1)
+        else:
+            ref = spa.attention(*full)
         torch.cuda.synchronize()
         out = torch.empty((B, bounds[rank + 1] - bounds[rank], H, D), dtype=torch.bfloat16, device="cuda") \
             if src else None
@@ -56,6 +64,8 @@ def run(rank: int, world: int, port: int, case: dict, errq):
                 out.fill_(0)
             if qkv_mode:
                 spa.spa_pipesp_qkv_attention(plan, C, x_r, wp, out, ws)
+            elif ring:
+                spa.spa_ring_attention(plan, *shard, out, ws)
             elif case.get("n_src"):
                 spa.spa_aco_attention(plan, *shard, out, ws)
             elif case.get("ulysses"):

@@ -4,7 +4,8 @@ maps the others' workspaces through CUDA IPC and the exchange is ordered by cros
 another GPU over NVLink in production), this is the multi-GPU code path: separate CUDA contexts, separate streams,
 peer pointers, no shared host state.  Every rank's output must equal the single-GPU kernel bit for bit, on every
 call of the same plan (the epochs advance), for the staged copy-engine exchange and the direct (kernel-store)
-transport, PipeSP / Ulysses / Aco / the fused QKV projection."""
+transport, PipeSP / Ulysses / Aco / the fused QKV projection, and Ring-Attention (bit-identical to the same ring
+over virtual ranks on one GPU)."""
 import socket
 
 import pytest
@@ -56,6 +57,9 @@ _port_cache = [0]
     (4, dict(B=1, S=3000, H=8, D=128, stages=2, n_src=3, direct=True)),
     (2, dict(B=1, S=2048, H=4, D=128, stages=2, qkv=True)),       # f3 over the P2P transport
     (8, dict(B=1, S=8192, H=24, D=128, stages=3)),
+    (2, dict(B=1, S=2048, H=3, D=128, ring=True)),                # Ring-Attention over P2P (R21, any H)
+    (4, dict(B=2, S=4096, H=5, D=64, ring=True)),
+    (8, dict(B=1, S=8192, H=24, D=96, ring=True)),
 ])
 def test_p2p_processes_bit_identical(world, case):
     _port_cache[0] = _port()
