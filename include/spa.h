@@ -232,6 +232,20 @@ spa_status spa_plan_host_workspace_bytes(const spa_plan *plan, size_t *bytes);
 spa_status spa_attention_host(spa_plan *plan, const void *q, const void *k, const void *v, void *o, void *ws,
                               void *stream);
 
+/* The SP layer (spa_pipesp_attention) from and to HOST memory at any rank count (pinned host buffers for overlap):
+ * q, k, v, out = host [B, S_r, H, D] bf16 of this rank (loopback: one per source rank; Aco co-processor ranks pass
+ * NULL); ws = spa_plan_host_sp_workspace_bytes(): the plan's workspace followed by device copies of the local Q, K, V,
+ * O.  Per head group kh of the stage split: the H2D of its heads' columns (for every destination rank) runs on a copy
+ * stream and only group kh's pack waits for it; as soon as the last stage of group kh is exchanged back, its unpack
+ * and the D2H of its output columns run on a second copy stream -- the copies overlap the other groups' exchange and
+ * attention.  Same result bits as spa_pipesp_attention.  1-rank plans: spa_attention_host.  P2P plans: register this
+ * ws (spa_plan_ipc_handle / open).  Not for ring plans; SPA_OPT_DIRECT does not apply. */
+spa_status spa_plan_host_sp_workspace_bytes(const spa_plan *plan, size_t *bytes);
+spa_status spa_pipesp_attention_hostbuf(spa_plan *plan, const void *q, const void *k, const void *v, void *out,
+                                        void *ws, void *stream);
+spa_status spa_pipesp_attention_hostbuf_local(spa_plan *plan, const void *const q[], const void *const k[],
+                                              const void *const v[], void *const out[], void *ws, void *stream);
+
 /* ------------------------------------------------------------------ QKV projection fused with PipeSP
  * The SP layer from the hidden states ("after each GPU computes its portion of the sub-sequence's
  * Q, K, and V, three rounds of All-to-All ..."; the projections Q = X W_Q, K = X W_K, V = X W_V of PAPER.md:155-157,

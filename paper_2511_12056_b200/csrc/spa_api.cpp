@@ -147,6 +147,7 @@ struct spa_plan {
     bool p2p_flush = false;
     int attn_launches = 0, copy_launches = 0, gemm_launches = 0;
     cudaStream_t sc_alt = nullptr;  // second compute stream: odd stages, so stage k+1 fills stage k's wave tail
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;   // host-buffer SP calls: input / output copy streams
 };
 
 namespace {
@@ -256,7 +257,7 @@ int real_heads(const spa_plan *p, const Split &s, int q, int kh) {
 // One 4-level job when every head group is complete; with padded heads one job per (kh, q) that copies only
 // the real heads of the group (pad-head slots of the send buffer are never written nor read as results).
 void pack_jobs(const spa_plan *p, const Split &s, int r, const void *x, long long dst_off, uint8_t *ws,
-               std::vector<CopyJob> &out) {
+               std::vector<CopyJob> &out, int kh_only = -1) {
     const long long D2 = (long long)p->sh.D * 2, H = p->sh.H, n = p->len[r];   // source rank r: n tokens
     const long long run = s.g * D2;
     // x == NULL / ws == NULL (describe): the job pointers hold plain byte offsets
@@ -265,9 +266,10 @@ void pack_jobs(const spa_plan *p, const Split &s, int r, const void *x, long lon
     auto at = [](uintptr_t base, long long off) { return reinterpret_cast<uint8_t *>(base + (uintptr_t)off); };
     if (p->Hp == p->sh.H) {
         CopyJob j{};
-        j.src = at(xb, 0);
-        j.dst = at(wb, 0);
-        j.count[0] = s.G_h; j.count[1] = p->P; j.count[2] = p->sh.B; j.count[3] = n;
+        const int kh0 = kh_only < 0 ? 0 : kh_only;   // one head group only: its heads' runs for every destination
+        j.src = at(xb, kh0 * s.g * D2);
+        j.dst = at(wb, idx_send(p, s, r, kh0, 0, 0, 0) * 2);
+        j.count[0] = kh_only < 0 ? s.G_h : 1; j.count[1] = p->P; j.count[2] = p->sh.B; j.count[3] = n;
         j.src_stride[0] = s.g * D2; j.src_stride[1] = p->h * D2; j.src_stride[2] = n * H * D2;
         j.src_stride[3] = H * D2;
         j.dst_stride[3] = run; j.dst_stride[2] = n * run; j.dst_stride[1] = p->sh.B * n * run;
@@ -279,7 +281,7 @@ void pack_jobs(const spa_plan *p, const Split &s, int r, const void *x, long lon
     for (int kh = 0; kh < s.G_h; ++kh)
         for (int q = 0; q < p->P; ++q) {
             const int nreal = real_heads(p, s, q, kh);
-            if (nreal == 0) continue;
+            if (nreal == 0 || (kh_only >= 0 && kh != kh_only)) continue;
             CopyJob j{};
             j.src = at(xb, (q * p->h + kh * s.g) * D2);
             j.dst = at(wb, idx_send(p, s, r, kh, q, 0, 0) * 2);
@@ -292,9 +294,9 @@ void pack_jobs(const spa_plan *p, const Split &s, int r, const void *x, long lon
 }
 // Unpack (source rank), Psi_g fused: out[b][t][q*h + kh*g + jj][d] = orecv[kh][q][b][t][jj][d]  (a5)
 void unpack_jobs(const spa_plan *p, const Split &s, int r, uint8_t *ws, long long src_off, void *outp,
-                 std::vector<CopyJob> &out) {
+                 std::vector<CopyJob> &out, int kh_only = -1) {
     const size_t first = out.size();
-    pack_jobs(p, s, r, nullptr, 0, nullptr, out);
+    pack_jobs(p, s, r, nullptr, 0, nullptr, out, kh_only);
     for (size_t i = first; i < out.size(); ++i) {
         CopyJob &j = out[i];
         std::swap(j.src_stride, j.dst_stride);
@@ -371,6 +373,10 @@ struct Exec {  // everything one call needs
     std::vector<const void *> xin;
     const uint8_t *wp = nullptr;   // packed weight + bias (spa_plan_pack_qkv_weight)
     int C = 0;
+    // host-buffer SP call: pinned host q/k/v/out per local source; ptr.q/k/v/out are then the device staging copies
+    bool host = false;
+    std::vector<const void *> hq, hk, hv;
+    std::vector<void *> hout;
 };
 
 // ------------------------------------------------------------------ packed QKV weight
@@ -626,6 +632,69 @@ spa_status run_qkv_pack(Exec &x, cudaEvent_t *ev_gemm) {
                                (long long)s.g * p->sh.D, x.sc));
         }
         SPA_CHECK_CUDA(cudaEventRecord(ev_gemm[kh], x.sc));
+    }
+    return SPA_OK;
+}
+
+// Host-buffer calls: the columns of head group kh's heads (for every destination rank) of one host [B, S_r, H, D]
+// tensor, as 2-D copies (one per destination rank's head block); dir H2D or D2H.
+spa_status copy_group_columns(const spa_plan *p, const Split &s, int r, int kh, void *dst, const void *src,
+                              cudaMemcpyKind kind, cudaStream_t st) {
+    const size_t row = (size_t)p->sh.H * p->sh.D * 2;
+    for (int q = 0; q < p->P; ++q) {
+        const int nreal = real_heads(p, s, q, kh);
+        if (nreal == 0) continue;
+        const size_t off = ((size_t)q * p->h + (size_t)kh * s.g) * p->sh.D * 2;
+        SPA_CHECK_CUDA(cudaMemcpy2DAsync(reinterpret_cast<uint8_t *>(dst) + off, row,
+                                         reinterpret_cast<const uint8_t *>(src) + off, row,
+                                         (size_t)nreal * p->sh.D * 2, (size_t)p->sh.B * p->len[r], kind, st));
+    }
+    return SPA_OK;
+}
+
+// H2D of head group kh's Q/K/V columns on s_h2d, then its pack on the caller's stream; ev_ready[kh] = group kh's send
+// regions complete (the input exchange of its first chunk waits for it)
+spa_status run_host_pack(Exec &x, cudaEvent_t *ev_h2d, cudaEvent_t *ev_ready) {
+    spa_plan *p = x.p;
+    const Split &s = *x.s;
+    const int nr = (p->comm->kind == KIND_LOOPBACK) ? p->Psrc : (is_source(p, p->comm->rank) ? 1 : 0);
+    for (int kh = 0; kh < s.G_h; ++kh) {
+        std::vector<CopyJob> jobs;
+        for (int i = 0; i < nr; ++i) {
+            const int r = (p->comm->kind == KIND_LOOPBACK) ? i : p->comm->rank;
+            const void *hs[3] = {x.hq[i], x.hk[i], x.hv[i]};
+            const void *ds[3] = {x.ptr.q[i], x.ptr.k[i], x.ptr.v[i]};
+            for (int t = 0; t < 3; ++t)
+                SPA_TRY(copy_group_columns(p, s, r, kh, const_cast<void *>(ds[t]), hs[t], cudaMemcpyHostToDevice,
+                                           p->s_h2d));
+            uint8_t *ws = resolve(x, r, BUF_WS, 0);
+            pack_jobs(p, s, r, x.ptr.q[i], p->off_sendQ, ws, jobs, kh);
+            pack_jobs(p, s, r, x.ptr.k[i], p->off_sendK, ws, jobs, kh);
+            pack_jobs(p, s, r, x.ptr.v[i], p->off_sendV, ws, jobs, kh);
+        }
+        SPA_CHECK_CUDA(cudaEventRecord(ev_h2d[kh], p->s_h2d));
+        SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_h2d[kh], 0));
+        if (!jobs.empty()) SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sc, &p->copy_launches));
+        SPA_CHECK_CUDA(cudaEventRecord(ev_ready[kh], x.sc));
+    }
+    return SPA_OK;
+}
+
+// Output of head group kh once its last stage's exchange is complete: unpack + Psi_g (copy kernel) and D2H of its
+// columns, both on s_d2h (so neither waits behind later stages on the compute or comm streams)
+spa_status run_host_unpack(Exec &x, int kh) {
+    spa_plan *p = x.p;
+    const Split &s = *x.s;
+    const int nr = (p->comm->kind == KIND_LOOPBACK) ? p->Psrc : (is_source(p, p->comm->rank) ? 1 : 0);
+    std::vector<CopyJob> jobs;
+    for (int i = 0; i < nr; ++i) {
+        const int r = (p->comm->kind == KIND_LOOPBACK) ? i : p->comm->rank;
+        unpack_jobs(p, s, r, resolve(x, r, BUF_WS, 0), p->off_orecv, x.ptr.out[i], jobs, kh);
+    }
+    if (!jobs.empty()) SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), p->s_d2h, &p->copy_launches));
+    for (int i = 0; i < nr; ++i) {
+        const int r = (p->comm->kind == KIND_LOOPBACK) ? i : p->comm->rank;
+        SPA_TRY(copy_group_columns(p, s, r, kh, x.hout[i], x.ptr.out[i], cudaMemcpyDeviceToHost, p->s_d2h));
     }
     return SPA_OK;
 }
@@ -906,8 +975,8 @@ spa_status execute(Exec &x) {
     p->gemm_launches = 0;
     const Split &s = *x.s;
     const int N = s.n();
-    SPA_TRY(ensure_events(p, 4 + 3 * (size_t)N + s.G_h, p->profile ? 8 + 6 * (size_t)N : 0));
-    if (p->direct && p->P > 1 && x.has_attn && x.has_pack && x.has_out && !x.qkv)
+    SPA_TRY(ensure_events(p, 4 + 3 * (size_t)N + 3 * (size_t)s.G_h, p->profile ? 8 + 6 * (size_t)N : 0));
+    if (p->direct && p->P > 1 && x.has_attn && x.has_pack && x.has_out && !x.qkv && !x.host)
         return p->comm->kind == KIND_P2P ? execute_direct_p2p(x) : execute_direct(x);
     Prof pr{p};
     if (p->P == 1) {
@@ -954,6 +1023,14 @@ spa_status execute(Exec &x) {
     cudaEvent_t *ev = p->sync_ev.data();
     cudaEvent_t ev_entry = ev[0], ev_pack = ev[1], ev_done = ev[2];
     cudaEvent_t *ev_in = ev + 4, *ev_attn = ev + 4 + N, *ev_out = ev + 4 + 2 * N, *ev_gemm = ev + 4 + 3 * N;
+    cudaEvent_t *ev_h2d = ev_gemm + s.G_h, *ev_hout = ev_gemm + 2 * s.G_h;
+    if (x.host) {
+        if (!p->s_h2d) SPA_CHECK_CUDA(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
+        if (!p->s_d2h) SPA_CHECK_CUDA(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
+        SPA_CHECK_CUDA(cudaEventRecord(ev_entry, x.sc));
+        SPA_CHECK_CUDA(cudaStreamWaitEvent(p->s_h2d, ev_entry, 0));
+        SPA_CHECK_CUDA(cudaStreamWaitEvent(p->s_d2h, ev_entry, 0));
+    }
 
     pr.begin("total", x.sc);
     SPA_CHECK_CUDA(cudaEventRecord(ev_entry, x.sc));
@@ -966,16 +1043,18 @@ spa_status execute(Exec &x) {
     if (x.has_pack) {
         pr.begin("pack", x.sc);
         if (x.qkv) SPA_TRY(run_qkv_pack(x, ev_gemm));
+        else if (x.host) SPA_TRY(run_host_pack(x, ev_h2d, ev_gemm));
         else SPA_TRY(run_pack(x));
         pr.end("pack", x.sc);
     }
     SPA_CHECK_CUDA(cudaEventRecord(ev_pack, x.sc));
-    // the staged pack is one launch; the fused projections complete head group by head group (ev_gemm)
-    if (!x.qkv) SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_pack, 0));
+    // the staged pack is one launch; the fused projections / host copies complete head group by head group (ev_gemm)
+    const bool per_group = x.qkv || x.host;
+    if (!per_group) SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_pack, 0));
 
     auto issue_in = [&](int k) -> spa_status {
         NvtxRange r_in("spa: input exchange");
-        if (x.qkv && k % s.C == 0) SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_gemm[k / s.C], 0));
+        if (per_group && k % s.C == 0) SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_gemm[k / s.C], 0));
         const std::string nm = "in" + std::to_string(k);
         pr.begin(nm, x.sm);
         SPA_TRY(run_exchange(x, k, 0));
@@ -1002,10 +1081,19 @@ spa_status execute(Exec &x) {
             SPA_TRY(run_exchange(x, k, 1));
             pr.end(on, x.sm);
             SPA_CHECK_CUDA(cudaEventRecord(ev_out[k], x.sm));
+            if (x.host && k % s.C == s.C - 1) {   // head group k / C complete: its output goes home now
+                const int kh = k / s.C;
+                SPA_CHECK_CUDA(cudaStreamWaitEvent(p->s_d2h, ev_out[k], 0));
+                if (p2p && !p->skip_comm)
+                    for (int kk = kh * s.C; kk <= k; ++kk) SPA_TRY(p2p_wait(p, p->s_d2h, FLAG_OUT, kk));
+                SPA_TRY(run_host_unpack(x, kh));
+                SPA_CHECK_CUDA(cudaEventRecord(ev_hout[kh], p->s_d2h));
+            }
             if (k + 2 < N) SPA_TRY(issue_in(k + 2));
         }
         SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_out[N - 1], 0));
-        if (p2p && !p->skip_comm)
+        if (x.host) SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_hout[s.G_h - 1], 0));
+        if (p2p && !p->skip_comm && !x.host)
             for (int k = 0; k < N; ++k) SPA_TRY(p2p_wait(p, x.sc, FLAG_OUT, k));   // every owner's output rows
     } else if (!x.has_out) {
         // reshard seq->head: the one input exchange only
@@ -1019,7 +1107,7 @@ spa_status execute(Exec &x) {
         SPA_CHECK_CUDA(cudaEventRecord(ev_out[0], x.sm));
         SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_out[0], 0));
     }
-    if (x.has_out) {
+    if (x.has_out && !x.host) {
         pr.begin("unpack", x.sc);
         SPA_TRY(run_unpack(x));
         pr.end("unpack", x.sc);
@@ -1524,6 +1612,8 @@ spa_status spa_plan_destroy(spa_plan *plan) {
     for (auto e : plan->sync_ev) cudaEventDestroy(e);
     for (auto e : plan->prof_ev) cudaEventDestroy(e);
     if (plan->sc_alt) cudaStreamDestroy(plan->sc_alt);
+    if (plan->s_h2d) cudaStreamDestroy(plan->s_h2d);
+    if (plan->s_d2h) cudaStreamDestroy(plan->s_d2h);
     delete plan;
     return SPA_OK;
 }
@@ -2050,6 +2140,59 @@ spa_status spa_attention_host(spa_plan *p, const void *q, const void *k, const v
     SPA_CHECK_CUDA(cudaEventRecord(ev_done, s_out));
     SPA_CHECK_CUDA(cudaStreamWaitEvent(sc, ev_done, 0));
     return SPA_OK;
+}
+
+// ------------------------------------------------------------------ SP layer from / to host buffers (e2e at any N)
+static long long host_sp_staging_off(const spa_plan *p) {
+    const long long per = p->ws_rank_bytes;
+    return align_up(p->comm->kind == KIND_LOOPBACK ? per * p->P : per, 256);
+}
+static long long host_sp_tensor_bytes(const spa_plan *p) { return align_up((long long)p->sh.B * p->S_l * p->sh.H * p->sh.D * 2, 256); }
+
+spa_status spa_plan_host_sp_workspace_bytes(const spa_plan *plan, size_t *bytes) {
+    if (!plan || !bytes) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (plan->ring) return fail(SPA_ERR_UNSUPPORTED, "host-buffer SP calls: Ulysses / PipeSP / Aco plans");
+    if (plan->P == 1) return spa_plan_host_workspace_bytes(plan, bytes);
+    const int nloc = plan->comm->kind == KIND_LOOPBACK ? plan->Psrc : 1;
+    *bytes = (size_t)(host_sp_staging_off(plan) + 4LL * nloc * host_sp_tensor_bytes(plan));
+    return SPA_OK;
+}
+
+static spa_status host_sp_call(spa_plan *p, int n, const void *const q[], const void *const k[], const void *const v[],
+                               void *const out[], void *ws, void *stream, bool local) {
+    if (!p) return fail(SPA_ERR_INVALID, "plan is NULL");
+    if (p->ring) return fail(SPA_ERR_UNSUPPORTED, "host-buffer SP calls: Ulysses / PipeSP / Aco plans");
+    if (p->P == 1) {
+        if (n != 1 || !q[0] || !k[0] || !v[0] || !out[0]) return fail(SPA_ERR_INVALID, "NULL argument");
+        return spa_attention_host(p, q[0], k[0], v[0], out[0], ws, stream);
+    }
+    Exec e{};
+    SPA_TRY(prepare(p, e, ws, stream, local));
+    e.s = &p->split;
+    e.host = true;
+    uint8_t *stage = reinterpret_cast<uint8_t *>(ws) + host_sp_staging_off(p);
+    const long long T = host_sp_tensor_bytes(p);
+    for (int i = 0; i < n; ++i) {
+        if (!q[i] || !k[i] || !v[i] || !out[i]) return fail(SPA_ERR_INVALID, "NULL host buffer");
+        e.hq.push_back(q[i]); e.hk.push_back(k[i]); e.hv.push_back(v[i]); e.hout.push_back(out[i]);
+        uint8_t *d = stage + 4LL * i * T;   // device staging copies of this source's Q, K, V, O
+        e.ptr.q.push_back(d); e.ptr.k.push_back(d + T); e.ptr.v.push_back(d + 2 * T); e.ptr.out.push_back(d + 3 * T);
+    }
+    return execute(e);
+}
+
+spa_status spa_pipesp_attention_hostbuf(spa_plan *plan, const void *q, const void *k, const void *v, void *out,
+                                        void *ws, void *stream) {
+    if (plan && plan->Psrc != plan->P && !is_source(plan, plan->comm->rank)) {   // Aco co-processor: no buffers
+        if (q || k || v || out) return fail(SPA_ERR_INVALID, "co-processor ranks pass NULL q/k/v/out");
+        return host_sp_call(plan, 0, nullptr, nullptr, nullptr, nullptr, ws, stream, false);
+    }
+    return host_sp_call(plan, 1, &q, &k, &v, &out, ws, stream, false);
+}
+spa_status spa_pipesp_attention_hostbuf_local(spa_plan *plan, const void *const q[], const void *const k[],
+                                              const void *const v[], void *const out[], void *ws, void *stream) {
+    if (!plan || !q || !k || !v || !out) return fail(SPA_ERR_INVALID, "NULL argument");
+    return host_sp_call(plan, n_local_srcs(plan), q, k, v, out, ws, stream, true);
 }
 
 spa_status spa_ring_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out, void *ws,

@@ -23,6 +23,7 @@ __all__ = [
     "BUF_WS", "SPA_OPT_PROFILE", "SPA_OPT_SKIP_COMM", "SPA_OPT_COPROC_BUSY", "SPA_OPT_DIRECT", "SPA_OPT_COMM_SMS",
     "SPA_OPT_RANK_ONLY", "SPA_OPT_LOOPBACK_CE",
     "spa_pipesp_qkv_attention", "spa_pipesp_qkv_attention_local", "spa_qkv_projection",
+    "spa_pipesp_attention_hostbuf", "spa_pipesp_attention_hostbuf_local",
 ]
 
 SPA_OPT_PROFILE, SPA_OPT_SKIP_COMM, SPA_OPT_COPROC_BUSY, SPA_OPT_DIRECT, SPA_OPT_COMM_SMS = 1, 2, 3, 4, 5
@@ -125,6 +126,9 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "spa_aco_attention_local": ([_P, _PP, _PP, _PP, _PP, _P, _P], i),
         "spa_ring_attention": ([_P, _P, _P, _P, _P, _P, _P], i),
         "spa_attention_host": ([_P, _P, _P, _P, _P, _P, _P], i),
+        "spa_plan_host_sp_workspace_bytes": ([_P, ctypes.POINTER(ctypes.c_size_t)], i),
+        "spa_pipesp_attention_hostbuf": ([_P, _P, _P, _P, _P, _P, _P], i),
+        "spa_pipesp_attention_hostbuf_local": ([_P, _PP, _PP, _PP, _PP, _P, _P], i),
         "spa_plan_host_workspace_bytes": ([_P, ctypes.POINTER(ctypes.c_size_t)], i),
         "spa_ring_attention_local": ([_P, _PP, _PP, _PP, _PP, _P, _P], i),
         "spa_reshard_seq_to_head": ([_P, _P, _P, _P, _P], i),
@@ -301,6 +305,12 @@ class Plan:
         p = Profile()
         _check(load().spa_plan_last_profile(self.h, ctypes.byref(p)), "spa_plan_last_profile")
         return p
+
+    @property
+    def host_sp_workspace_bytes(self) -> int:
+        n = ctypes.c_size_t()
+        _check(load().spa_plan_host_sp_workspace_bytes(self.h, ctypes.byref(n)), "spa_plan_host_sp_workspace_bytes")
+        return n.value
 
     @property
     def host_workspace_bytes(self) -> int:
@@ -486,6 +496,17 @@ def spa_attention_host(plan: Plan, q, k, v, o, ws, stream=None):
     """q, k, v, o: host (pinned) bf16 [B, S, H, D] tensors; ws: device workspace of plan.host_workspace_bytes."""
     _check(load().spa_attention_host(plan.h, _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(ws), _stream(stream)),
            "spa_attention_host")
+
+
+def spa_pipesp_attention_hostbuf(plan: Plan, q, k, v, out, ws, stream=None):
+    """q, k, v, out: this rank's pinned host bf16 [B, S_r, H, D] (None on Aco co-processor ranks)."""
+    _check(load().spa_pipesp_attention_hostbuf(plan.h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(ws),
+                                               _stream(stream)), "spa_pipesp_attention_hostbuf")
+
+
+def spa_pipesp_attention_hostbuf_local(plan: Plan, qs, ks, vs, outs, ws, stream=None):
+    _check(load().spa_pipesp_attention_hostbuf_local(plan.h, _arr(qs), _arr(ks), _arr(vs), _arr(outs), _ptr(ws),
+                                                     _stream(stream)), "spa_pipesp_attention_hostbuf_local")
 
 
 def spa_ring_attention(plan: Plan, q, k, v, out, ws, stream=None):

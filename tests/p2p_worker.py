@@ -31,7 +31,8 @@ def run(rank: int, world: int, port: int, case: dict, errq):
                         n_src=case.get("n_src", 0), ring=ring)
         if case.get("direct"):
             plan.set_option(spa.SPA_OPT_DIRECT, 1)
-        ws = plan.workspace()
+        ws = torch.empty(plan.host_sp_workspace_bytes, dtype=torch.uint8, device="cuda") if case.get("hostbuf") \
+            else plan.workspace()
         plan.ipc_setup(ws)
         qkv_mode = case.get("qkv", False)
         if qkv_mode:
@@ -62,7 +63,14 @@ def run(rank: int, world: int, port: int, case: dict, errq):
         for it in range(case.get("calls", 3)):
             if out is not None:
                 out.fill_(0)
-            if qkv_mode:
+            if case.get("hostbuf"):   # pinned host buffers in and out (spa_pipesp_attention_hostbuf)
+                hq = [x.cpu().pin_memory() if x is not None else None for x in shard]
+                hout = torch.zeros(out.shape, dtype=out.dtype).pin_memory() if src else None
+                spa.spa_pipesp_attention_hostbuf(plan, *hq, hout, ws)
+                torch.cuda.synchronize()
+                if src:
+                    out.copy_(hout)
+            elif qkv_mode:
                 spa.spa_pipesp_qkv_attention(plan, C, x_r, wp, out, ws)
             elif ring:
                 spa.spa_ring_attention(plan, *shard, out, ws)

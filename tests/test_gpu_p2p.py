@@ -60,6 +60,8 @@ _port_cache = [0]
     (2, dict(B=1, S=2048, H=3, D=128, ring=True)),                # Ring-Attention over P2P (R21, any H)
     (4, dict(B=2, S=4096, H=5, D=64, ring=True)),
     (8, dict(B=1, S=8192, H=24, D=96, ring=True)),
+    (4, dict(B=1, S=4096, H=8, D=128, stages=4, hostbuf=True)),   # host buffers in / out, pipelined per group
+    (4, dict(B=1, S=3000, H=8, D=64, stages=2, n_src=3, hostbuf=True)),
 ])
 def test_p2p_processes_bit_identical(world, case):
     _port_cache[0] = _port()

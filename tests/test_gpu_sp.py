@@ -244,3 +244,28 @@ def test_rank_only_measurement_mode():
     torch.cuda.synchronize()
     prof = plan.last_profile()
     assert prof.attn_launches == 2 and prof.n_stages == 2
+
+
+@pytest.mark.parametrize("P,stages,B,S,H,D,n_src,pad", [
+    (2, 2, 1, 1024, 4, 64, 0, False), (4, 4, 2, 2048, 8, 128, 0, False), (4, 8, 1, 2051, 8, 96, 0, False),
+    (8, 3, 1, 4096, 24, 128, 0, False), (8, 3, 1, 4096, 24, 64, 6, False), (3, 2, 1, 960, 4, 64, 0, True),
+    (1, 4, 1, 1024, 8, 64, 0, False),
+])
+def test_hostbuf_sp_equals_device_call(P, stages, B, S, H, D, n_src, pad):
+    """spa_pipesp_attention_hostbuf(_local): pinned host Q/K/V in, host O out, H2D / exchange / attention / D2H
+    pipelined per head group -- the same bits as the single-GPU kernel (and so as the device-buffer SP call)."""
+    q, k, v = (synthgen.gen_qkv_shard(3, t, (B, S, H, D), 0, S, device="cuda") for t in range(3))
+    single = spa.attention(q, k, v)
+    torch.cuda.synchronize()
+    nsrc = n_src or P
+    b = osp.shard_bounds(S, nsrc)
+    plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=stages, n_src=n_src, pad_heads=pad)
+    hs = [[x[:, b[r]:b[r + 1]].cpu().pin_memory() for r in range(nsrc)] for x in (q, k, v)]
+    houts = [torch.zeros((B, b[r + 1] - b[r], H, D), dtype=torch.bfloat16).pin_memory() for r in range(nsrc)]
+    ws = torch.empty(plan.host_sp_workspace_bytes, dtype=torch.uint8, device="cuda")
+    for _ in range(2):   # the same buffers twice (no state left behind)
+        for o in houts:
+            o.zero_()
+        spa.spa_pipesp_attention_hostbuf_local(plan, *hs, houts, ws)
+        torch.cuda.synchronize()
+        assert torch.equal(torch.cat(houts, dim=1).view(torch.int16), single.cpu().view(torch.int16))
