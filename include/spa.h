@@ -203,7 +203,7 @@ spa_status spa_plan_last_profile(spa_plan *plan, spa_profile *out);
 /* ------------------------------------------------------------------ SP attention (per-rank collective calls)
  * q, k, v, out: device bf16 [B, S/n_src, H, D] contiguous (this rank's shard); ws: device
  * workspace of spa_plan_workspace_bytes(); stream: cudaStream_t of the caller.
- * NCCL plans only (loopback plans use the *_local variants). */
+ * NCCL or P2P plans (loopback plans use the *_local variants). */
 spa_status spa_ulysses_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out,
                                  void *ws, void *stream);
 spa_status spa_pipesp_attention(spa_plan *plan, const void *q, const void *k, const void *v, void *out,

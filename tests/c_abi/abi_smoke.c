@@ -48,6 +48,21 @@ int main(void) {
     CHECK(sent > 0 && sent == recvd, "stage 0 sends == receives for a uniform plan");
     spa_attn_desc a;
     CHECK(spa_plan_describe_attention(plan, 0, 3, &a) == SPA_OK && a.Skv == 118800 && a.n_heads == 1, "attn desc");
+    /* the fused QKV projection's packed weight: 3 head groups of 3*8*1*128 rows of C, + fp32 bias */
+    size_t wb = 0;
+    CHECK(spa_plan_qkv_weight_bytes(plan, 3072, &wb) == SPA_OK && wb >= (size_t)9216 * 3072 * 2 + 9216 * 4, "qkv w");
+    CHECK(spa_plan_qkv_weight_bytes(plan, 3071, &wb) == SPA_ERR_SHAPE, "C % 8 rejected");
+    /* host-buffer SP workspace = the plan's + device copies of this rank's Q, K, V, O */
+    size_t hb = 0;
+    CHECK(spa_plan_host_sp_workspace_bytes(plan, &hb) == SPA_OK && hb >= ws + (size_t)4 * 14850 * 24 * 128 * 2, "hostbuf ws");
+    CHECK(spa_plan_destroy(plan) == SPA_OK, "destroy plan");
+    /* a ring plan: step 0 of rank 3 sends K, V to rank 4 and receives from rank 2 */
+    spa_shape rs;
+    memset(&rs, 0, sizeof rs);
+    rs.B = 1; rs.S = 8 * 64; rs.H = 5; rs.D = 64; rs.stages = 1; rs.ring = 1;
+    CHECK(spa_plan_create(&plan, comm, &rs) == SPA_OK, "ring plan");
+    CHECK(spa_plan_describe_ring(plan, 0, 3, msgs, 64, &nm) == SPA_OK && nm == 4 && msgs[0].peer == 4 &&
+              msgs[2].peer == 2 && msgs[2].is_recv, "ring step");
     CHECK(spa_plan_destroy(plan) == SPA_OK && spa_comm_destroy(comm) == SPA_OK, "destroy");
     printf("c abi ok: %s\n", spa_version());
     return 0;
