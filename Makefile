@@ -18,7 +18,7 @@ $(LIBDIR)/%.o: $(CSRC)/%.cu $(CSRC)/ptx.cuh $(CSRC)/spa_internal.h include/spa.h
 
 $(LIBDIR)/spa_api.o: $(CSRC)/spa_api.cpp $(CSRC)/spa_internal.h include/spa.h
 	@mkdir -p $(LIBDIR)
-	$(NVCC) -O3 -std=c++17 -Xcompiler -fPIC,-O3 -I$(NCCL)/include -Iinclude -c $< -o $@
+	$(NVCC) $(ARCH) -O3 -std=c++17 -Xcompiler -fPIC,-O3 -I$(NCCL)/include -Iinclude -c $< -o $@
 
 $(LIBDIR)/libspa.so: $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL)/lib -l:libnccl.so.2 -Xlinker=-rpath=$(NCCL)/lib \

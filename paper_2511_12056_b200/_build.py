@@ -65,7 +65,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False, varia
         obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + tag + ".o")
         cmd = common + ["-x", "cu" if src.endswith(".cu") else "c++", "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cpp"):
-            cmd = [nvcc(), "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O3", f"-I{inc}",
+            cmd = [nvcc(), *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O3", f"-I{inc}",
                    f"-I{os.path.join(ROOT, 'include')}", "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
