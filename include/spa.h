@@ -66,7 +66,10 @@ typedef struct spa_plan spa_plan;
 /* ------------------------------------------------------------------ rank groups */
 /* NCCL unique id (128 bytes) created on rank 0; the caller broadcasts it (torch.distributed). */
 spa_status spa_get_unique_id(uint8_t id[128]);
-/* One process per GPU: NCCL communicator of `nranks` ranks over NVLink/NVSwitch; `device` = CUDA ordinal. */
+/* One process per GPU: NCCL communicator of `nranks` ranks over NVLink/NVSwitch; `device` = CUDA ordinal.
+ * Validation status: the NCCL message lists are matched across ranks on the host and exchanged over
+ * gloo, a 1-rank NCCL communicator runs on the GPU; the multi-GPU NCCL exchange itself has not run in this build's
+ * one-GPU test environment -- the P2P transport (spa_comm_init_p2p) has, with real processes. */
 spa_status spa_comm_init(spa_comm **comm, const uint8_t id[128], int nranks, int rank, int device);
 /* The same with NCCL communicator settings: the SM budget of NCCL's kernels while the attention grid occupies the
  * GPU (ncclConfig_t minCTAs / maxCTAs / CTAPolicy; NCCL 2.28).  0 leaves a field at NCCL's default (and its env
