@@ -62,6 +62,9 @@ _port_cache = [0]
     (8, dict(B=1, S=8192, H=24, D=96, ring=True)),
     (4, dict(B=1, S=4096, H=8, D=128, stages=4, hostbuf=True)),   # host buffers in / out, pipelined per group
     (4, dict(B=1, S=3000, H=8, D=64, stages=2, n_src=3, hostbuf=True)),
+    # full size (configs[3]: 720p, 8 processes, N_st = 3), staged copy engines and direct stores
+    (8, dict(B=1, S=118_800, H=24, D=128, stages=3, calls=2)),
+    (8, dict(B=1, S=118_800, H=24, D=128, stages=3, calls=2, direct=True)),
 ])
 def test_p2p_processes_bit_identical(world, case):
     _port_cache[0] = _port()
