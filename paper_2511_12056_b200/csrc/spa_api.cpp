@@ -147,6 +147,10 @@ struct spa_plan {
     bool p2p_flush = false;
     int attn_launches = 0, copy_launches = 0, gemm_launches = 0;
     cudaStream_t sc_alt = nullptr;  // second compute stream: odd stages, so stage k+1 fills stage k's wave tail
+    // stage window W (SPA_OPT_STAGE_WINDOW): up to W stages' attention in flight on W compute streams (the caller's, sc_alt,
+    // then extra_streams); the comm stream issues in(0..W-1) up front and in(k+W) after out(k)
+    int stage_window = 4;   // measured (profiles/r02/stage_window): flat at 720p, up to 1.8x at OSP with 24 stages
+    std::vector<cudaStream_t> extra_streams;
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;   // host-buffer SP calls: input / output copy streams
 };
 
@@ -424,6 +428,21 @@ uint8_t *resolve(const Exec &x, int rank, int buf, long long off) {
         case BUF_K: return (uint8_t *)x.ptr.k[idx] + off;
         default: return (uint8_t *)x.ptr.v[idx] + off;
     }
+}
+
+// Compute stream of stage k: the caller's, sc_alt, then the plan's extra streams, round-robin over the stage window.
+spa_status stage_stream(spa_plan *p, cudaStream_t sc, int k, cudaStream_t *out) {
+    const int w = std::max(1, p->stage_window), i = k % w;
+    if (i == 0) { *out = sc; return SPA_OK; }
+    if (!p->sc_alt) SPA_CHECK_CUDA(cudaStreamCreateWithFlags(&p->sc_alt, cudaStreamNonBlocking));
+    if (i == 1) { *out = p->sc_alt; return SPA_OK; }
+    while ((int)p->extra_streams.size() < i - 1) {
+        cudaStream_t st;
+        SPA_CHECK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        p->extra_streams.push_back(st);
+    }
+    *out = p->extra_streams[i - 2];
+    return SPA_OK;
 }
 
 // ------------------------------------------------------------------ P2P transport (CUDA IPC peer memory)
@@ -812,7 +831,9 @@ spa_status execute_direct(Exec &x) {
         const int kh = k / s.C, c = k % s.C;
         const long long Lst = Lstage(p, s, c);
         const std::string an = "attn" + std::to_string(k);
-        cudaStream_t st = (k & 1) ? p->sc_alt : x.sc;
+        cudaStream_t st;
+        SPA_TRY(stage_stream(p, x.sc, k, &st));
+        if (st != x.sc && st != p->sc_alt) SPA_CHECK_CUDA(cudaStreamWaitEvent(st, ev_pack, 0));
         pr.begin(an, st);
         for (int r = 0; r < p->P; ++r) {   // owner r
             if (p->rank_only >= 0 && r != p->rank_only) continue;
@@ -846,6 +867,10 @@ spa_status execute_direct(Exec &x) {
     }
     SPA_CHECK_CUDA(cudaEventRecord(ev_alt, p->sc_alt));
     SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_alt, 0));
+    for (cudaStream_t st : p->extra_streams) {   // join the wider stage window (the event is reused in order)
+        SPA_CHECK_CUDA(cudaEventRecord(ev_alt, st));
+        SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_alt, 0));
+    }
     pr.end("total", x.sc);
     finish_profile(p, pr, N);
     return SPA_OK;
@@ -919,7 +944,9 @@ spa_status execute_direct_p2p(Exec &x) {
         const int kh = k / s.C, c = k % s.C;
         const long long Lst = Lstage(p, s, c);
         const std::string an = "attn" + std::to_string(k);
-        cudaStream_t st = (k & 1) ? p->sc_alt : x.sc;
+        cudaStream_t st;
+        SPA_TRY(stage_stream(p, x.sc, k, &st));
+        if (st != x.sc && st != p->sc_alt) SPA_CHECK_CUDA(cudaStreamWaitEvent(st, ev_pack, 0));
         pr.begin(an, st);
         const int nreal = real_heads(p, s, me, kh);
         if (nreal > 0) {
@@ -951,6 +978,10 @@ spa_status execute_direct_p2p(Exec &x) {
     }
     SPA_CHECK_CUDA(cudaEventRecord(ev_alt, p->sc_alt));
     SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_alt, 0));
+    for (cudaStream_t st : p->extra_streams) {   // join the wider stage window (the event is reused in order)
+        SPA_CHECK_CUDA(cudaEventRecord(ev_alt, st));
+        SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_alt, 0));
+    }
     if (!p->skip_comm) {
         SPA_TRY(p2p_signal(p, x.sc, FLAG_OUT, 0));   // this owner's rows are in every source's landing buffer
         SPA_TRY(p2p_wait(p, x.sc, FLAG_OUT, 0));
@@ -1063,10 +1094,11 @@ spa_status execute(Exec &x) {
         return SPA_OK;
     };
     if (x.has_attn) {
-        SPA_TRY(issue_in(0));
-        if (N > 1) SPA_TRY(issue_in(1));
+        const int W = std::max(1, p->stage_window);
+        for (int k = 0; k < std::min(W, N); ++k) SPA_TRY(issue_in(k));
         for (int k = 0; k < N; ++k) {
-            cudaStream_t st = (k & 1) ? x.sc_alt : x.sc;
+            cudaStream_t st;
+            SPA_TRY(stage_stream(p, x.sc, k, &st));
             NvtxRange r_stage("spa: stage");
             SPA_CHECK_CUDA(cudaStreamWaitEvent(st, ev_in[k], 0));
             if (p2p && !p->skip_comm) SPA_TRY(p2p_wait(p, st, FLAG_IN, k));   // the peers' pieces of stage k
@@ -1089,7 +1121,7 @@ spa_status execute(Exec &x) {
                 SPA_TRY(run_host_unpack(x, kh));
                 SPA_CHECK_CUDA(cudaEventRecord(ev_hout[kh], p->s_d2h));
             }
-            if (k + 2 < N) SPA_TRY(issue_in(k + 2));
+            if (k + W < N) SPA_TRY(issue_in(k + W));
         }
         SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_out[N - 1], 0));
         if (x.host) SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_hout[s.G_h - 1], 0));
@@ -1612,6 +1644,7 @@ spa_status spa_plan_destroy(spa_plan *plan) {
     for (auto e : plan->sync_ev) cudaEventDestroy(e);
     for (auto e : plan->prof_ev) cudaEventDestroy(e);
     if (plan->sc_alt) cudaStreamDestroy(plan->sc_alt);
+    for (cudaStream_t st : plan->extra_streams) cudaStreamDestroy(st);
     if (plan->s_h2d) cudaStreamDestroy(plan->s_h2d);
     if (plan->s_d2h) cudaStreamDestroy(plan->s_d2h);
     delete plan;
@@ -1636,6 +1669,10 @@ spa_status spa_plan_set_option(spa_plan *plan, int option, int value) {
         case SPA_OPT_LOOPBACK_CE:
             if (plan->comm->kind != KIND_LOOPBACK) return fail(SPA_ERR_INVALID, "loopback plans only");
             plan->loopback_ce = value != 0;
+            break;
+        case SPA_OPT_STAGE_WINDOW:
+            if (value < 1 || value > 8) return fail(SPA_ERR_INVALID, "stage window must be in [1, 8]");
+            plan->stage_window = value;
             break;
         case SPA_OPT_COMM_SMS:
             if (value < 0 || value > 64) return fail(SPA_ERR_INVALID, "comm SMs must be in [0, 64]");

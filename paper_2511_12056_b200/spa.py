@@ -21,13 +21,13 @@ __all__ = [
     "spa_reshard_seq_to_head", "spa_reshard_head_to_seq", "spa_reshard_seq_to_head_local",
     "spa_reshard_head_to_seq_local", "spa_pad_heads", "attention", "BUF_Q", "BUF_K", "BUF_V", "BUF_OUT",
     "BUF_WS", "SPA_OPT_PROFILE", "SPA_OPT_SKIP_COMM", "SPA_OPT_COPROC_BUSY", "SPA_OPT_DIRECT", "SPA_OPT_COMM_SMS",
-    "SPA_OPT_RANK_ONLY", "SPA_OPT_LOOPBACK_CE",
+    "SPA_OPT_RANK_ONLY", "SPA_OPT_LOOPBACK_CE", "SPA_OPT_STAGE_WINDOW",
     "spa_pipesp_qkv_attention", "spa_pipesp_qkv_attention_local", "spa_qkv_projection",
     "spa_pipesp_attention_hostbuf", "spa_pipesp_attention_hostbuf_local",
 ]
 
 SPA_OPT_PROFILE, SPA_OPT_SKIP_COMM, SPA_OPT_COPROC_BUSY, SPA_OPT_DIRECT, SPA_OPT_COMM_SMS = 1, 2, 3, 4, 5
-SPA_OPT_RANK_ONLY, SPA_OPT_LOOPBACK_CE = 6, 7
+SPA_OPT_RANK_ONLY, SPA_OPT_LOOPBACK_CE, SPA_OPT_STAGE_WINDOW = 6, 7, 8
 BUF_Q, BUF_K, BUF_V, BUF_OUT, BUF_WS = 0, 1, 2, 3, 4
 HEADER = os.path.join(os.path.dirname(_build.HERE), "include", "spa.h")
 

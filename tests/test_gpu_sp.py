@@ -269,3 +269,21 @@ def test_hostbuf_sp_equals_device_call(P, stages, B, S, H, D, n_src, pad):
         spa.spa_pipesp_attention_hostbuf_local(plan, *hs, houts, ws)
         torch.cuda.synchronize()
         assert torch.equal(torch.cat(houts, dim=1).view(torch.int16), single.cpu().view(torch.int16))
+
+
+@pytest.mark.parametrize("window,direct", [(1, False), (4, False), (8, False), (4, True)])
+def test_stage_window_bit_identical(window, direct):
+    """SPA_OPT_STAGE_WINDOW: 1..8 stages in flight on as many compute streams -- the same bits as the single kernel."""
+    B, S, H, D, P = 1, 2048, 24, 64, 8
+    q, k, v = (synthgen.gen_qkv_shard(4, t, (B, S, H, D), 0, S, device="cuda") for t in range(3))
+    single = spa.attention(q, k, v)
+    S_l = S // P
+    shards = [[x[:, i * S_l:(i + 1) * S_l].contiguous() for i in range(P)] for x in (q, k, v)]
+    outs = [torch.empty_like(t) for t in shards[0]]
+    plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=24)
+    plan.set_option(spa.SPA_OPT_STAGE_WINDOW, window)
+    if direct:
+        plan.set_option(spa.SPA_OPT_DIRECT, 1)
+    spa.spa_pipesp_attention_local(plan, *shards, outs, plan.workspace())
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(outs, 1).view(torch.int16), single.view(torch.int16))

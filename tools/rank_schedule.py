@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--modes", default="skip,kernel,ce,direct")
     ap.add_argument("--reps", type=int, default=7)
     ap.add_argument("--qkv", action="store_true", help="layer from hidden states (fused QKV projection, f3)")
+    ap.add_argument("--window", type=int, default=4, help="SPA_OPT_STAGE_WINDOW (stages in flight)")
     ap.add_argument("--aco", type=int, default=0,
                     help="Aco plan: n_src source ranks of P (PAPER.md:150-199); --rank may name a co-processor")
     ap.add_argument("--peak", type=float, default=None, help="bf16 TF/s (default MEASURED_PEAKS.json)")
@@ -80,6 +81,7 @@ def main():
             raise SystemExit("--qkv plans have no co-processor ranks")
         for st in [int(x) for x in args.stages.split(",")]:
             plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=st, n_src=args.aco)
+            plan.set_option(spa.SPA_OPT_STAGE_WINDOW, args.window)
             ws = plan.qkv_workspace() if args.qkv else plan.workspace()
             wp = plan.pack_qkv_weight(W, bias) if args.qkv else None
             nbytes = sent_bytes(plan, r)
@@ -125,7 +127,7 @@ def main():
                 pm = prof[len(prof) // 2]
                 res[mode] = ms
                 t_roof = max((attn_flops_rank + proj_flops_rank) / (peak * 1e12), nbytes / 900e9) * 1e3
-                rec = {"workload": name, "P": P, "n_src": nsrc, "rank": r, "stages": st, "stage_split": list(plan.stage_split),
+                rec = {"workload": name, "P": P, "n_src": nsrc, "rank": r, "stages": st, "window": args.window, "stage_split": list(plan.stage_split),
                        "mode": mode, "qkv": args.qkv, "ms_per_layer": ms,
                        "tflops_per_gpu": (attn_flops_rank + proj_flops_rank) / (ms * 1e-3) / 1e12,
                        "tflops_aggregate_if_P_gpus": P * (attn_flops_rank + proj_flops_rank) / (ms * 1e-3) / 1e12,
