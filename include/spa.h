@@ -178,7 +178,7 @@ spa_status spa_plan_destroy(spa_plan *plan);
  *                          (wave tails, copy/attention SM contention); the output is then NOT the attention result
  *   SPA_OPT_LOOPBACK_CE 1 -> loopback exchange messages as copy-engine cudaMemcpyAsync (the P2P transport's staged
  *                          exchange) instead of the copy kernel (NCCL-like: SMs move the bytes); same result bits */
-/*   SPA_OPT_STAGE_WINDOW w -> up to w pipeline stages in flight (1..8, default 2): their attention launches go to w
+/*   SPA_OPT_STAGE_WINDOW w -> up to w pipeline stages in flight (1..8, default 4): their attention launches go to w
  *                          compute streams round-robin and the input exchange runs w stages ahead; wider windows keep
  *                          the GPU full when stages are small (many stages of a short sequence); same result bits */
 enum { SPA_OPT_PROFILE = 1, SPA_OPT_SKIP_COMM = 2, SPA_OPT_COPROC_BUSY = 3, SPA_OPT_DIRECT = 4, SPA_OPT_COMM_SMS = 5,
