@@ -41,6 +41,8 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
 }
 // Wait for the phase with the given parity to complete.  A watchdog turns a lost
 // arrival (a bug) into a trapped kernel instead of a hung GPU (~4 s).
+#define SPA_STR_(x) #x
+#define SPA_STR(x) SPA_STR_(x)
 #ifndef SPA_FAST_WAIT
 #define SPA_FAST_WAIT 1   // A/B (profiles/r02/attn_fastwait_ab.jsonl): HY-76k +1.0 % over 3 interleaved rounds, others within noise
 #endif
@@ -52,7 +54,11 @@ __device__ __forceinline__ bool mbar_try_wait_burst(uint64_t *bar, uint32_t pari
         "{\n\t.reg .pred p;\n\t.reg .u32 i;\n\t"
         "mov.u32 i, %3;\n\t"
         "SPA_WAIT_%=:\n\t"
+#ifdef SPA_WAIT_HINT_NS
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, " SPA_STR(SPA_WAIT_HINT_NS) ";\n\t"
+#else
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+#endif
         "@p bra.uni SPA_DONE_%=;\n\t"
         "sub.u32 i, i, 1;\n\t"
         "setp.ne.u32 p, i, 0;\n\t"
