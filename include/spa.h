@@ -95,8 +95,9 @@ spa_status spa_comm_init_loopback(spa_comm **comm, int nvirtual, int device);
  * SPA_OPT_DIRECT makes the pack kernel and the attention epilogue store to the peers themselves.  Cross-process
  * order: per-call epoch flags in each workspace's tail, written with cuStreamWriteValue32 (system-scope fence
  * first) after the data and awaited with cuStreamWaitValue32 -- no kernel ever spins on a flag.  Ulysses / PipeSP /
- * Aco / QKV / Ring plans (the ring's K/V blocks travel by copy engine into the next rank's receive slot, with
- * arrival and slot-free flags); no USP or reshard calls.  `rank` and `nranks` come from the caller's launcher. */
+ * Aco / QKV / Ring / USP plans and the reshard calls (the ring's K/V blocks travel by copy engine into the next
+ * rank's receive slot, with arrival and slot-free flags; a USP plan's Ulysses and ring sub-groups are mapped by its
+ * own spa_plan_ipc_open).  `rank` and `nranks` come from the caller's launcher. */
 spa_status spa_comm_init_p2p(spa_comm **comm, int nranks, int rank, int device);
 /* Host-only rank group: plans can be created, validated and described (spa_plan_describe_*),
  * but not executed.  Used to test the multi-rank host logic without a GPU. */

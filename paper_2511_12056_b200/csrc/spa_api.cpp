@@ -117,6 +117,7 @@ struct spa_plan {
     spa_plan *uly_plan = nullptr, *ring_plan = nullptr;
     long long ws_total = -1;                     // >= 0: spa_plan_workspace_bytes returns this
     long long off_kvbuf = 0, off_parts = 0, off_lse = 0;
+    long long off_ring_ws = -1;   // USP over P2P: the ring sub-plan's own workspace (the Ulysses one is at off_parts)
     Split split;
     // per-rank workspace layout (bytes)
     long long E_src = 0, E_own = 0;  // elements of one send-side / owner-side tensor
@@ -1131,6 +1132,11 @@ spa_status execute(Exec &x) {
         // reshard seq->head: the one input exchange only
         SPA_TRY(issue_in(0));
         SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_in[0], 0));
+        if (p2p) {   // the pieces landed in this rank's recvQ region ([B][S][h][D]): to the caller's x_head
+            if (!p->skip_comm) SPA_TRY(p2p_wait(p, x.sc, FLAG_IN, 0));
+            SPA_CHECK_CUDA(cudaMemcpyAsync(x.ptr.xhead[0], resolve(x, p->comm->rank, BUF_WS, p->off_recvQ),
+                                           (size_t)p->E_own * 2, cudaMemcpyDeviceToDevice, x.sc));
+        }
     } else {
         // reshard head->seq: the one output exchange only
         pr.begin("out0", x.sm);
@@ -1138,6 +1144,7 @@ spa_status execute(Exec &x) {
         pr.end("out0", x.sm);
         SPA_CHECK_CUDA(cudaEventRecord(ev_out[0], x.sm));
         SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sc, ev_out[0], 0));
+        if (p2p && !p->skip_comm) SPA_TRY(p2p_wait(p, x.sc, FLAG_OUT, 0));
     }
     if (x.has_out && !x.host) {
         pr.begin("unpack", x.sc);
@@ -1219,6 +1226,9 @@ static spa_status create_usp_plan(spa_plan **plan, spa_comm *comm, const spa_sha
     } else if (comm->kind == KIND_HOST) {
         st = spa_comm_init_host(&p->uly_comm, U, comm->rank % U);
         if (st == SPA_OK) st = spa_comm_init_host(&p->ring_comm, R, comm->rank / U);
+    } else if (comm->kind == KIND_P2P) {   // sub-groups of the same processes; mapped by spa_plan_ipc_open
+        st = spa_comm_init_p2p(&p->uly_comm, U, comm->rank % U, comm->device);
+        if (st == SPA_OK) st = spa_comm_init_p2p(&p->ring_comm, R, comm->rank / U, comm->device);
     } else {
         st = spa_comm_split(comm, comm->rank / U, comm->rank % U, &p->uly_comm);
         if (st == SPA_OK) st = spa_comm_split(comm, comm->rank % U, comm->rank / U, &p->ring_comm);
@@ -1235,7 +1245,12 @@ static spa_status create_usp_plan(spa_plan **plan, spa_comm *comm, const spa_sha
     const int nloc = comm->kind == KIND_LOOPBACK ? P : 1;
     p->off_kvbuf = 0;   // head-sharded Q, K, V, O per (local) rank: [nloc][4][E_loc] bf16
     p->off_parts = align_up((long long)nloc * 4 * p->E_loc * 2, 256);   // sub-plan workspace
-    p->ws_total = p->off_parts + (long long)std::max(wu, wr);
+    if (comm->kind == KIND_P2P) {   // separate regions: each sub-plan's epoch flags persist across calls
+        p->off_ring_ws = align_up(p->off_parts + (long long)wu, 256);
+        p->ws_total = p->off_ring_ws + (long long)wr;
+    } else {
+        p->ws_total = p->off_parts + (long long)std::max(wu, wr);
+    }
     *plan = p;
     return SPA_OK;
 }
@@ -1261,11 +1276,12 @@ static spa_status usp_call(spa_plan *p, const void *const q[], const void *const
     };
     uint8_t *w = reinterpret_cast<uint8_t *>(ws);
     uint8_t *sub_ws = w + p->off_parts;
+    uint8_t *ring_ws = p->off_ring_ws >= 0 ? w + p->off_ring_ws : sub_ws;
     auto head = [&](int i, int t) { return w + ((long long)i * 4 + t) * p->E_loc * 2; };   // t: 0 Q 1 K 2 V 3 O
     const void *const *in[3] = {q, k, v};
     if (!local) {
         for (int t = 0; t < 3; ++t) SPA_TRY(spa_reshard_seq_to_head(p->uly_plan, in[t][0], head(0, t), sub_ws, stream));
-        SPA_TRY(spa_ring_attention(p->ring_plan, head(0, 0), head(0, 1), head(0, 2), head(0, 3), sub_ws, stream));
+        SPA_TRY(spa_ring_attention(p->ring_plan, head(0, 0), head(0, 1), head(0, 2), head(0, 3), ring_ws, stream));
         SPA_TRY(spa_reshard_head_to_seq(p->uly_plan, head(0, 3), out[0], sub_ws, stream));
         return done();
     }
@@ -1440,6 +1456,21 @@ spa_status spa_plan_ipc_open(spa_plan *plan, void *ws, const uint8_t *handles) {
     cudaGetLastError();
     plan->peer_ws = peers;
     plan->epoch = 0;
+    if (plan->U > 1) {   // USP: the sub-plans' peers are the group's / ring's ranks, at the sub-plan offsets
+        const int U = plan->U, R = plan->R, u = me % U, rho = me / U;
+        spa_plan *up = plan->uly_plan, *rp = plan->ring_plan;
+        up->peer_ws.assign(U, nullptr);
+        rp->peer_ws.assign(R, nullptr);
+        for (int i = 0; i < U; ++i) up->peer_ws[i] = peers[rho * U + i] + plan->off_parts;
+        for (int i = 0; i < R; ++i) rp->peer_ws[i] = peers[i * U + u] + plan->off_ring_ws;
+        up->epoch = rp->epoch = 0;
+        up->p2p_flush = rp->p2p_flush = plan->p2p_flush;
+        if (up->P > 1)
+            SPA_CHECK_CUDA(cudaMemset(up->peer_ws[u] + up->off_flags, 0, (size_t)flag_bytes(up)));
+        if (rp->P > 1)
+            SPA_CHECK_CUDA(cudaMemset(rp->peer_ws[rho] + rp->off_flags, 0, (size_t)flag_bytes(rp)));
+        return SPA_OK;
+    }
     // this rank's flags start at 0 (the caller synchronises all ranks after ipc_open, before the first call)
     SPA_CHECK_CUDA(cudaMemset(reinterpret_cast<uint8_t *>(ws) + plan->off_flags, 0, (size_t)flag_bytes(plan)));
     return SPA_OK;
@@ -1548,8 +1579,6 @@ spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *sha
     if (s.ulysses < 0 || (!s.ring && s.ulysses > 1)) return fail(SPA_ERR_INVALID, "ulysses degree needs ring = 1");
     if (s.ring && (s.stages != 1 || s.pad_heads != 0))
         return fail(SPA_ERR_INVALID, "ring / USP plans take stages = 1 and pad_heads = 0");
-    if (s.ring && s.ulysses > 1 && comm->kind == KIND_P2P)
-        return fail(SPA_ERR_UNSUPPORTED, "USP plans need an NCCL or loopback comm");
     if (s.ring && s.ulysses > 1) return create_usp_plan(plan, comm, s);
     if (s.ring) {
         // Ring attention: every rank keeps all heads; only S % P matters.
@@ -2085,8 +2114,6 @@ static spa_status ring_call(spa_plan *p, int n, const void *const q[], const voi
 static spa_status reshard_call(spa_plan *plan, int n, const void *const x[], void *const xh[], void *ws, void *stream,
                                bool local, bool to_head) {
     if (plan && plan->ring) return fail(SPA_ERR_INVALID, "ring plan: no reshard");
-    if (plan && plan->comm->kind == KIND_P2P)   // the receive side is the caller's x_head, not a mapped workspace
-        return fail(SPA_ERR_UNSUPPORTED, "p2p plans: reshard calls need an NCCL or loopback comm");
     Exec e{};
     SPA_TRY(prepare(plan, e, ws, stream, local));
     if (plan->Psrc != plan->P) return fail(SPA_ERR_INVALID, "reshard needs n_src == nranks");
@@ -2104,7 +2131,9 @@ static spa_status reshard_call(spa_plan *plan, int n, const void *const x[], voi
     }
     if (to_head) {
         e.has_out = false;
-        e.q_recv_buf = BUF_XHEAD;
+        // P2P: peers can only write into mapped workspaces -- receive into this rank's recvQ region ([B][S][h][D] for
+        // one stage) and copy it to x_head locally (execute)
+        e.q_recv_buf = plan->comm->kind == KIND_P2P ? BUF_WS : BUF_XHEAD;
     } else {
         e.has_pack = false;
         e.o_send_buf = BUF_XHEAD;

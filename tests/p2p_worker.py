@@ -26,9 +26,10 @@ def run(rank: int, world: int, port: int, case: dict, errq):
         for r in range(n_src):
             bounds.append(bounds[-1] + S // n_src + (1 if r < S % n_src else 0))
         src = rank < n_src
-        ring = case.get("ring", False)
+        usp = case.get("usp", 0)   # Ulysses degree of a USP plan (ring over the groups)
+        ring = case.get("ring", False) or usp > 1
         plan = spa.Plan(spa.Comm.p2p(world, rank, 0), B, S, H, D, stages=case.get("stages", 1),
-                        n_src=case.get("n_src", 0), ring=ring)
+                        n_src=case.get("n_src", 0), ring=ring, ulysses=usp)
         if case.get("direct"):
             plan.set_option(spa.SPA_OPT_DIRECT, 1)
         ws = torch.empty(plan.host_sp_workspace_bytes, dtype=torch.uint8, device="cuda") if case.get("hostbuf") \
@@ -49,7 +50,7 @@ def run(rank: int, world: int, port: int, case: dict, errq):
             full = [synthgen.gen_qkv_shard(case.get("seed", 0), t, (B, S, H, D), 0, S, device="cuda")
                     for t in range(3)]
         if ring:   # the ring's reference bits: the same plan over `world` virtual ranks on one GPU (R21)
-            lp = spa.Plan(spa.Comm.loopback(world), B, S, H, D, ring=True)
+            lp = spa.Plan(spa.Comm.loopback(world), B, S, H, D, ring=True, ulysses=usp)
             parts = [[x[:, bounds[r]:bounds[r + 1]].contiguous() for r in range(world)] for x in full]
             louts = [torch.empty_like(t) for t in parts[0]]
             spa.spa_ring_attention_local(lp, *parts, louts, lp.workspace())

@@ -4,8 +4,8 @@ maps the others' workspaces through CUDA IPC and the exchange is ordered by cros
 another GPU over NVLink in production), this is the multi-GPU code path: separate CUDA contexts, separate streams,
 peer pointers, no shared host state.  Every rank's output must equal the single-GPU kernel bit for bit, on every
 call of the same plan (the epochs advance), for the staged copy-engine exchange and the direct (kernel-store)
-transport, PipeSP / Ulysses / Aco / the fused QKV projection, and Ring-Attention (bit-identical to the same ring
-over virtual ranks on one GPU)."""
+transport, PipeSP / Ulysses / Aco / the fused QKV projection, and Ring-Attention / USP (bit-identical to the same
+plan over virtual ranks on one GPU)."""
 import socket
 
 import pytest
@@ -62,6 +62,8 @@ _port_cache = [0]
     (8, dict(B=1, S=8192, H=24, D=96, ring=True)),
     (4, dict(B=1, S=4096, H=8, D=128, stages=4, hostbuf=True)),   # host buffers in / out, pipelined per group
     (4, dict(B=1, S=3000, H=8, D=64, stages=2, n_src=3, hostbuf=True)),
+    (4, dict(B=1, S=4096, H=8, D=128, usp=2)),                    # USP: Ulysses in pairs x Ring over 2 groups
+    (8, dict(B=1, S=8192, H=12, D=64, usp=4)),
     # full size (configs[3]: 720p, 8 processes, N_st = 3), staged copy engines and direct stores
     (8, dict(B=1, S=118_800, H=24, D=128, stages=3, calls=2)),
     (8, dict(B=1, S=118_800, H=24, D=128, stages=3, calls=2, direct=True)),
