@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--stages", type=int, default=0, help="N_st (0 = paper's per-head loop, h stages)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--host-groups", type=int, default=8, help="head groups of the 1-GPU host-buffer e2e call")
+    ap.add_argument("--host-groups", type=int, default=24, help="head groups of the 1-GPU host-buffer e2e call")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
     ap.add_argument("--spawn", action="store_true", help="launch through torch.distributed.run even at N=1")

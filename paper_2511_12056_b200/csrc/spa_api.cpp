@@ -2163,8 +2163,8 @@ spa_status spa_attention_host(spa_plan *p, const void *q, const void *k, const v
     cudaStream_t sc = reinterpret_cast<cudaStream_t>(stream);
     SPA_TRY(ensure_stream(p->comm));
     cudaStream_t s_out = p->comm->stream;
-    if (!p->sc_alt) SPA_CHECK_CUDA(cudaStreamCreateWithFlags(&p->sc_alt, cudaStreamNonBlocking));
-    cudaStream_t s_in = p->sc_alt;
+    if (!p->s_h2d) SPA_CHECK_CUDA(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
+    cudaStream_t s_in = p->s_h2d;
     const int B = p->sh.B, S = p->sh.S, H = p->sh.H, D = p->sh.D;
     const int G = p->split.G_h, g = H / G;   // head groups (stages = head-group count; query chunks unused)
     SPA_TRY(ensure_events(p, 4 + 2 * (size_t)G, 0));
@@ -2189,16 +2189,19 @@ spa_status spa_attention_host(spa_plan *p, const void *q, const void *k, const v
         SPA_CHECK_CUDA(cudaEventRecord(ev_in[i], s_in));
     }
     for (int i = 0; i < G; ++i) {
-        SPA_CHECK_CUDA(cudaStreamWaitEvent(sc, ev_in[i], 0));
+        // group i's attention on compute stream i mod W (stage window): later groups fill earlier groups' wave tails
+        cudaStream_t st;
+        SPA_TRY(stage_stream(p, sc, i, &st));
+        SPA_CHECK_CUDA(cudaStreamWaitEvent(st, ev_in[i], 0));
         AttnProblem a{};
         a.q = dX[0] + i * group; a.k = dX[1] + i * group; a.v = dX[2] + i * group; a.o = dX[3] + i * group;
         a.B = B; a.Sq = a.Skv = S; a.n_heads = g; a.D = D;
         a.q_tok_stride = a.kv_tok_stride = a.o_tok_stride = (long long)g * D;
         a.q_batch_stride = a.kv_batch_stride = a.o_batch_stride = (long long)S * g * D;
         a.kv_len = p->kv_len;
-        SPA_CHECK_CUDA(launch_attention(a, sc));
+        SPA_CHECK_CUDA(launch_attention(a, st));
         ++p->attn_launches;
-        SPA_CHECK_CUDA(cudaEventRecord(ev_comp[i], sc));
+        SPA_CHECK_CUDA(cudaEventRecord(ev_comp[i], st));
         SPA_CHECK_CUDA(cudaStreamWaitEvent(s_out, ev_comp[i], 0));
         SPA_CHECK_CUDA(cudaMemcpy2DAsync(reinterpret_cast<uint8_t *>(o) + i * grow, row, dX[3] + i * group, grow, grow,
                                          rows, cudaMemcpyDeviceToHost, s_out));
