@@ -153,8 +153,9 @@ struct Cfg {
 #ifdef SPA_POLY_FROM
     static constexpr int POLY_FROM = SPA_POLY_FROM;
 #else
-    // sweeps (profiles/r01_v5_experiments): 1/4 on the FMA pipe is best at D=128, 1/8 at D=96 (+~2 %, noisy)
-    static constexpr int POLY_FROM = (D == 96) ? 14 : 12;
+    // 1/4 on the FMA pipe at every D: interleaved in-process A/B (tools/ab.py, profiles/r02/softmax_ceiling/): at D=96
+    // 1/4 beats 1/8 by 1.4-2.5 % (three boxes), 3/8 is equal, 1/2 worse; at D=64 3/8 and 1/8 are 1-2 % slower
+    static constexpr int POLY_FROM = 12;
 #endif
     static_assert(SMEM_BYTES + XCH_BYTES <= 227 * 1024, "shared memory");
     static_assert(NS <= 16, "barrier block");
