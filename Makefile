@@ -7,7 +7,8 @@ NCCL    ?= $(shell $(PYTHON) -c "import nvidia.nccl as n; print(list(n.__path__)
 ARCH    := -gencode arch=compute_100a,code=sm_100a
 CSRC    := paper_2511_12056_b200/csrc
 LIBDIR  := paper_2511_12056_b200/lib
-OBJS    := $(LIBDIR)/attn_fwd.o $(LIBDIR)/qkv_gemm.o $(LIBDIR)/reshard.o $(LIBDIR)/lse_merge.o $(LIBDIR)/spa_api.o
+OBJS    := $(LIBDIR)/attn_fwd.o $(LIBDIR)/qkv_gemm.o $(LIBDIR)/reshard.o $(LIBDIR)/lse_merge.o $(LIBDIR)/nccl_window.o \
+           $(LIBDIR)/spa_api.o
 CUFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -I$(NCCL)/include -Iinclude
 
 all: $(LIBDIR)/libspa.so

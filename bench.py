@@ -49,9 +49,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
     ap.add_argument("--spawn", action="store_true", help="launch through torch.distributed.run even at N=1")
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
-                    help="N>1 exchange: NCCL grouped send/recv, or CUDA IPC peer memory with copy engines (f1)")
-    ap.add_argument("--direct", action="store_true", help="p2p transport: pack / epilogue store to peers (f1)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p", "nccl-window"],
+                    help="N>1 exchange: NCCL grouped send/recv; CUDA IPC peer memory with copy engines (f1); or the "
+                         "same peer-memory exchange on an NCCL symmetric window (ncclMemAlloc + ncclCommWindowRegister)")
+    ap.add_argument("--direct", action="store_true",
+                    help="p2p / nccl-window transports: pack / epilogue store to peers (f1)")
     ap.add_argument("--qkv", action="store_true",
                     help="layer from hidden states: fused QKV projection (f3) + PipeSP; FLOPs include the projection")
     ap.add_argument("--north-star", type=int, default=-1,
@@ -297,6 +299,10 @@ def run_ours(args):
     def p2p_setup(plan, ws):
         if P > 1 and args.transport == "p2p":   # map every rank's workspace (CUDA IPC handles over torch.distributed)
             plan.ipc_setup(ws)
+            if args.direct:
+                plan.set_option(spa.SPA_OPT_DIRECT, 1)
+        elif P > 1 and args.transport == "nccl-window":   # a window of ws's size from NCCL's allocator replaces ws
+            ws = plan.window_setup(ws.numel())
             if args.direct:
                 plan.set_option(spa.SPA_OPT_DIRECT, 1)
         return ws

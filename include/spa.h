@@ -157,6 +157,28 @@ spa_status spa_plan_workspace_bytes(const spa_plan *plan, size_t *bytes);
 #define SPA_IPC_HANDLE_BYTES 72
 spa_status spa_plan_ipc_handle(spa_plan *plan, void *ws, uint8_t handle[SPA_IPC_HANDLE_BYTES]);
 spa_status spa_plan_ipc_open(spa_plan *plan, void *ws, const uint8_t *handles);
+/* NCCL plans on NCCL symmetric-memory windows (NCCL >= 2.28; SURVEY f1 on NVLink / NVSwitch): the exchange then
+ * runs on peer memory exactly as for P2P plans -- copy-engine copies of every message straight into the receivers'
+ * regions, or with SPA_OPT_DIRECT the pack kernel's and the attention epilogue's stores into the peers -- ordered by
+ * the same per-call epoch flags, instead of NCCL send / recv.  Set-up, once per plan:
+ *   1. every rank: spa_mem_alloc(bytes, &ws) with bytes >= spa_plan_workspace_bytes(plan) rounded up to 4096
+ *      (ncclMemAlloc: the memory NCCL can map into its peers)
+ *   2. every rank: spa_plan_window_register(plan, ws) -- COLLECTIVE over the plan's communicator
+ *      (ncclCommWindowRegister, NCCL_WIN_COLL_SYMMETRIC); resolves every rank's address of its window with NCCL's
+ *      device API (ncclGetLsaPointer) and zeroes this rank's flags.  SPA_ERR_COMM if a rank is outside the caller's
+ *      NVLink domain; SPA_ERR_UNSUPPORTED for ring / USP plans (they keep NCCL send / recv); 1-rank plans: no-op.
+ *   3. a host barrier over all ranks before the first call
+ * Afterwards every call passes this ws; spa_plan_destroy deregisters the window; spa_mem_free(ws) after that.
+ * SPA_OPT_DIRECT on an NCCL plan requires the window (SPA_ERR_INVALID at the call otherwise).  Validation status:
+ * the peer-memory execution is the P2P transport's (multi-process tested); the window plumbing is checked on one
+ * GPU by spa_comm_window_selftest; an NCCL exchange between several GPUs has not run in this build's environment. */
+spa_status spa_mem_alloc(size_t bytes, void **ptr);
+spa_status spa_mem_free(void *ptr);
+spa_status spa_plan_window_register(spa_plan *plan, void *ws);
+/* One-GPU check of the window plumbing on an NCCL comm (collective): ncclMemAlloc `bytes` (a multiple of 4096),
+ * register them as a symmetric window, resolve every rank's LSA address on the device, store a pattern through THIS
+ * rank's LSA address with a kernel and read it back through the local pointer; SPA_OK iff every word matches. */
+spa_status spa_comm_window_selftest(spa_comm *comm, size_t bytes);
 /* G_h, C, g of the plan's stage split. */
 spa_status spa_plan_stage_split(const spa_plan *plan, int *G_h, int *C, int *g);
 spa_status spa_plan_destroy(spa_plan *plan);
@@ -171,7 +193,8 @@ spa_status spa_plan_destroy(spa_plan *plan);
 /*   SPA_OPT_DIRECT    1 -> direct transport: the pack stores straight into the
  *                          owners' receive regions and the attention epilogue stores each output row straight
  *                          into its source rank's output (no staging, exchange copies or unpack).  Loopback
- *                          plans only for now (the NVLink version needs registered NCCL windows); same bits. */
+ *                          plans, P2P plans, and NCCL plans with a registered window (spa_plan_window_register);
+ *                          same bits. */
 /*   SPA_OPT_COMM_SMS  n -> the persistent QKV-projection GEMM (spa_pipesp_qkv_attention*) leaves n SMs free so that
  *                          the communication kernels of the overlapped all-to-alls get SMs at once (0..64; default 0) */
 /*   SPA_OPT_RANK_ONLY r+1 -> loopback plans: only virtual rank r's launches and the messages it sends or receives

@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libspa.so")
 TRACE_LIB = os.path.join(LIBDIR, "libspa_trace.so")
-SOURCES = ["attn_fwd.cu", "qkv_gemm.cu", "reshard.cu", "lse_merge.cu", "spa_api.cpp"]
+SOURCES = ["attn_fwd.cu", "qkv_gemm.cu", "reshard.cu", "lse_merge.cu", "nccl_window.cu", "spa_api.cpp"]
 HEADERS = ["ptx.cuh", "spa_internal.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -142,6 +142,9 @@ struct spa_plan {
     // flags in each workspace's tail order the cross-process exchange (ready[src], in[k][src], out[k][src], uint32)
     std::vector<uint8_t *> peer_ws;   // [P]; own entry = the registered local workspace
     std::vector<void *> ipc_bases;    // opened peer allocations (closed by spa_plan_destroy)
+    // NCCL plans with a registered symmetric window (spa_plan_window_register): peer_ws from NCCL's LSA mapping, and
+    // the same peer-memory execution as P2P plans (copy engines / direct stores + epoch flags)
+    ncclWindow_t win = nullptr;
     uint32_t epoch = 0;
     long long off_flags = 0, off_outbuf = 0;
     int n_flag_stages = 1;
@@ -155,6 +158,10 @@ struct spa_plan {
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;   // host-buffer SP calls: input / output copy streams
 };
 
+namespace spa {
+cudaError_t nccl_window_bases(ncclWindow_t w, int n, uint8_t **bases, cudaStream_t st);   // nccl_window.cu
+cudaError_t nccl_window_fill_pattern(uint32_t *lsa_self, long long n_words, uint32_t seed, cudaStream_t st);
+}  // namespace spa
 namespace {
 
 // ------------------------------------------------------------------ stage split (R7)
@@ -416,12 +423,15 @@ spa_status launch_qkv(spa_plan *p, const void *x, const uint8_t *wp, int C, int 
     return SPA_OK;
 }
 
+// The exchange runs on peer memory: CUDA-IPC (P2P) plans, and NCCL plans with a registered symmetric window.
+bool peer_mem(const spa_plan *p) { return p->comm->kind == KIND_P2P || p->win != nullptr; }
+
 uint8_t *resolve(const Exec &x, int rank, int buf, long long off) {
     const spa_plan *p = x.p;
     int idx = (p->comm->kind == KIND_LOOPBACK) ? rank : 0;
     switch (buf) {
         case BUF_WS:
-            if (p->comm->kind == KIND_P2P) return p->peer_ws[rank] + off;   // own or a peer's (CUDA IPC mapping)
+            if (peer_mem(p)) return p->peer_ws[rank] + off;   // own or a peer's (CUDA IPC or NCCL window mapping)
             return x.ptr.ws + (p->comm->kind == KIND_LOOPBACK ? (long long)rank * p->ws_rank_bytes : 0) + off;
         case BUF_XHEAD: return reinterpret_cast<uint8_t *>(x.ptr.xhead[idx]) + off;
         case BUF_OUT: return reinterpret_cast<uint8_t *>(x.ptr.out[idx]) + off;
@@ -552,7 +562,7 @@ spa_status match_and_copy(Exec &x, int me, Gen gen, cudaStream_t st) {
 spa_status run_exchange(Exec &x, int k, int dir) {
     spa_plan *p = x.p;
     if (p->skip_comm) return SPA_OK;
-    if (p->comm->kind == KIND_P2P) {
+    if (peer_mem(p)) {
         auto gen = [&](int r, std::vector<Msg> &m) {
             if (dir == 0) gen_in_msgs(p, *x.s, k, r, x.in_tensors, x.q_recv_buf, m);
             else gen_out_msgs(p, *x.s, k, r, x.o_send_buf, m);
@@ -1009,7 +1019,7 @@ spa_status execute(Exec &x) {
     const int N = s.n();
     SPA_TRY(ensure_events(p, 4 + 3 * (size_t)N + 3 * (size_t)s.G_h, p->profile ? 8 + 6 * (size_t)N : 0));
     if (p->direct && p->P > 1 && x.has_attn && x.has_pack && x.has_out && !x.qkv && !x.host)
-        return p->comm->kind == KIND_P2P ? execute_direct_p2p(x) : execute_direct(x);
+        return peer_mem(p) ? execute_direct_p2p(x) : execute_direct(x);
     Prof pr{p};
     if (p->P == 1) {
         // one rank owns everything: attention straight on the caller's [B,S,H,D] buffers
@@ -1067,7 +1077,7 @@ spa_status execute(Exec &x) {
     pr.begin("total", x.sc);
     SPA_CHECK_CUDA(cudaEventRecord(ev_entry, x.sc));
     SPA_CHECK_CUDA(cudaStreamWaitEvent(x.sm, ev_entry, 0));
-    const bool p2p = p->comm->kind == KIND_P2P;
+    const bool p2p = peer_mem(p);
     if (p2p) {   // a new epoch; no rank writes into a peer before that peer finished its previous call
         ++p->epoch;
         SPA_TRY(p2p_barrier(p, x.sm));
@@ -1175,6 +1185,10 @@ spa_status prepare(spa_plan *p, Exec &x, void *ws, void *stream, bool local) {
         if (p->peer_ws.empty()) return fail(SPA_ERR_INVALID, "p2p plan: call spa_plan_ipc_open first");
         if (ws != p->peer_ws[p->comm->rank]) return fail(SPA_ERR_INVALID, "p2p plan: ws is not the registered workspace");
     }
+    if (p->win && ws != p->peer_ws[p->comm->rank])
+        return fail(SPA_ERR_INVALID, "NCCL window plan: ws is not the registered window");
+    if (p->comm->kind == KIND_NCCL && p->direct && !p->win && p->P > 1)
+        return fail(SPA_ERR_INVALID, "direct transport on an NCCL plan: register the workspace (spa_plan_window_register)");
     x.p = p;
     x.ptr.ws = reinterpret_cast<uint8_t *>(ws);
     x.sc = reinterpret_cast<cudaStream_t>(stream);
@@ -1476,6 +1490,98 @@ spa_status spa_plan_ipc_open(spa_plan *plan, void *ws, const uint8_t *handles) {
     return SPA_OK;
 }
 
+// ------------------------------------------------------------------ NCCL symmetric windows (SURVEY f1 on NCCL plans)
+spa_status spa_mem_alloc(size_t bytes, void **ptr) {
+    if (!ptr || bytes == 0) return fail(SPA_ERR_INVALID, "spa_mem_alloc: NULL ptr or 0 bytes");
+    *ptr = nullptr;
+    SPA_CHECK_NCCL(ncclMemAlloc(ptr, bytes));
+    return SPA_OK;
+}
+
+spa_status spa_mem_free(void *ptr) {
+    if (!ptr) return SPA_OK;
+    SPA_CHECK_NCCL(ncclMemFree(ptr));
+    return SPA_OK;
+}
+
+spa_status spa_plan_window_register(spa_plan *plan, void *ws) {
+    if (!plan || !ws) return fail(SPA_ERR_INVALID, "NULL argument");
+    if (plan->comm->kind != KIND_NCCL || !plan->comm->nccl) return fail(SPA_ERR_INVALID, "not an NCCL plan");
+    if (plan->ring || plan->U > 1)
+        return fail(SPA_ERR_UNSUPPORTED, "NCCL window: Ulysses / PipeSP / Aco plans (ring plans exchange with NCCL)");
+    if (plan->win) return fail(SPA_ERR_INVALID, "NCCL window already registered");
+    if (plan->P == 1) return SPA_OK;   // nothing is exchanged
+    if (reinterpret_cast<uintptr_t>(ws) % NCCL_WIN_REQUIRED_ALIGNMENT)
+        return fail(SPA_ERR_INVALID, "NCCL window: ws must be 4096-byte aligned (spa_mem_alloc)");
+    SPA_CHECK_CUDA(cudaSetDevice(plan->comm->device));
+    const size_t bytes = (size_t)align_up(plan->ws_rank_bytes, NCCL_WIN_REQUIRED_ALIGNMENT);
+    ncclWindow_t w = nullptr;
+    SPA_CHECK_NCCL(ncclCommWindowRegister(plan->comm->nccl, ws, bytes, &w, NCCL_WIN_COLL_SYMMETRIC));
+    std::vector<uint8_t *> peers(plan->P, nullptr);
+    cudaStream_t st = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = nccl_window_bases(w, plan->P, peers.data(), st);
+    if (st) cudaStreamDestroy(st);
+    if (e != cudaSuccess) {
+        ncclCommWindowDeregister(plan->comm->nccl, w);
+        return fail(SPA_ERR_CUDA, std::string("NCCL window: resolving the peers' addresses: ") + cudaGetErrorString(e));
+    }
+    for (uint8_t *b : peers)
+        if (!b) {
+            ncclCommWindowDeregister(plan->comm->nccl, w);
+            return fail(SPA_ERR_COMM, "NCCL window: a rank is outside this NVLink domain (no LSA address)");
+        }
+    plan->win = w;
+    plan->peer_ws = peers;
+    plan->peer_ws[plan->comm->rank] = reinterpret_cast<uint8_t *>(ws);   // local calls use the caller's address
+    plan->epoch = 0;
+    int flush = 0;
+    if (cudaDeviceGetAttribute(&flush, static_cast<cudaDeviceAttr>(CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES),
+                               plan->comm->device) == cudaSuccess)
+        plan->p2p_flush = flush != 0;
+    cudaGetLastError();
+    // this rank's flags start at 0 (the caller synchronises all ranks after the registration, before the first call)
+    SPA_CHECK_CUDA(cudaMemset(reinterpret_cast<uint8_t *>(ws) + plan->off_flags, 0, (size_t)flag_bytes(plan)));
+    return SPA_OK;
+}
+
+spa_status spa_comm_window_selftest(spa_comm *comm, size_t bytes) {
+    if (!comm || comm->kind != KIND_NCCL || !comm->nccl) return fail(SPA_ERR_INVALID, "not an NCCL comm");
+    if (bytes < 4096 || bytes % 4096) return fail(SPA_ERR_INVALID, "bytes: a positive multiple of 4096");
+    SPA_CHECK_CUDA(cudaSetDevice(comm->device));
+    void *buf = nullptr;
+    SPA_CHECK_NCCL(ncclMemAlloc(&buf, bytes));
+    ncclWindow_t w = nullptr;
+    spa_status rc = SPA_OK;
+    ncclResult_t r = ncclCommWindowRegister(comm->nccl, buf, bytes, &w, NCCL_WIN_COLL_SYMMETRIC);
+    if (r != ncclSuccess) {
+        ncclMemFree(buf);
+        return fail(SPA_ERR_COMM, std::string("ncclCommWindowRegister: ") + ncclGetErrorString(r));
+    }
+    std::vector<uint8_t *> bases(comm->nranks, nullptr);
+    cudaStream_t st = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = nccl_window_bases(w, comm->nranks, bases.data(), st);
+    std::vector<uint32_t> host(bytes / 4);
+    if (e == cudaSuccess) e = nccl_window_fill_pattern(reinterpret_cast<uint32_t *>(bases[comm->rank]),
+                                                       (long long)(bytes / 4), 0x5eedu + comm->rank, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(host.data(), buf, bytes, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (st) cudaStreamDestroy(st);
+    if (e != cudaSuccess) {
+        rc = fail(SPA_ERR_CUDA, std::string("window self-test: ") + cudaGetErrorString(e));
+    } else {
+        for (size_t i = 0; i < host.size(); ++i)
+            if (host[i] != (((uint32_t)(i * 2654435761u)) ^ (0x5eedu + (uint32_t)comm->rank))) {
+                rc = fail(SPA_ERR_COMM, "window self-test: a store through the rank's LSA address is not visible locally");
+                break;
+            }
+    }
+    ncclCommWindowDeregister(comm->nccl, w);
+    ncclMemFree(buf);
+    return rc;
+}
+
 spa_status spa_comm_init_host(spa_comm **comm, int nranks, int rank) {
     if (!comm || nranks < 1 || rank < 0 || rank >= nranks) return fail(SPA_ERR_INVALID, "bad host comm arguments");
     spa_comm *c = new spa_comm;
@@ -1633,7 +1739,8 @@ spa_status spa_plan_create(spa_plan **plan, spa_comm *comm, const spa_shape *sha
         p->off_orecv = take(p->E_src);
         p->off_recvQ = take(p->E_own); p->off_recvK = take(p->E_own); p->off_recvV = take(p->E_own);
         p->off_O = take(p->E_own);
-        if (comm->kind == KIND_P2P) {   // epoch flags + the direct transport's output landing buffer
+        if (comm->kind != KIND_LOOPBACK) {   // epoch flags + the direct transport's output landing buffer (P2P plans;
+                                             // NCCL plans once a symmetric window is registered)
             p->n_flag_stages = p->split.n();
             p->off_flags = take((flag_bytes(p) + 1) / 2);
             p->off_outbuf = take((long long)s.B * p->S_l * s.H * s.D);
@@ -1670,6 +1777,7 @@ spa_status spa_plan_destroy(spa_plan *plan) {
     if (plan->uly_comm) spa_comm_destroy(plan->uly_comm);
     if (plan->ring_comm) spa_comm_destroy(plan->ring_comm);
     for (void *b : plan->ipc_bases) cudaIpcCloseMemHandle(b);
+    if (plan->win && plan->comm->nccl) ncclCommWindowDeregister(plan->comm->nccl, plan->win);
     for (auto e : plan->sync_ev) cudaEventDestroy(e);
     for (auto e : plan->prof_ev) cudaEventDestroy(e);
     if (plan->sc_alt) cudaStreamDestroy(plan->sc_alt);
@@ -1708,8 +1816,6 @@ spa_status spa_plan_set_option(spa_plan *plan, int option, int value) {
             plan->comm_sms = value;
             break;
         case SPA_OPT_DIRECT:
-            if (value && plan->comm->kind == KIND_NCCL)
-                return fail(SPA_ERR_UNSUPPORTED, "direct transport: NVLink windows not built yet (loopback only)");
             if (value && (plan->ring || plan->Psrc > kMaxDst))
                 return fail(SPA_ERR_UNSUPPORTED, "direct transport: PipeSP / Ulysses / Aco plans with <= 16 sources");
             plan->direct = value != 0;
@@ -2133,7 +2239,7 @@ static spa_status reshard_call(spa_plan *plan, int n, const void *const x[], voi
         e.has_out = false;
         // P2P: peers can only write into mapped workspaces -- receive into this rank's recvQ region ([B][S][h][D] for
         // one stage) and copy it to x_head locally (execute)
-        e.q_recv_buf = plan->comm->kind == KIND_P2P ? BUF_WS : BUF_XHEAD;
+        e.q_recv_buf = peer_mem(plan) ? BUF_WS : BUF_XHEAD;
     } else {
         e.has_pack = false;
         e.o_send_buf = BUF_XHEAD;

@@ -107,6 +107,10 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         "spa_comm_wait": ([_P, _P, i], i),
         "spa_plan_ipc_handle": ([_P, _P, ctypes.c_char_p], i),
         "spa_plan_ipc_open": ([_P, _P, ctypes.c_char_p], i),
+        "spa_mem_alloc": ([ctypes.c_size_t, _PP], i),
+        "spa_mem_free": ([_P], i),
+        "spa_plan_window_register": ([_P, _P], i),
+        "spa_comm_window_selftest": ([_P, ctypes.c_size_t], i),
         "spa_comm_split": ([_P, i, i, _PP], i),
         "spa_comm_check": ([_P], i),
         "spa_comm_destroy": ([_P], i),
@@ -263,6 +267,10 @@ class Comm:
     def check(self):
         _check(load().spa_comm_check(self.h), "spa_comm_check")
 
+    def window_selftest(self, nbytes: int = 1 << 20):
+        """NCCL comms, collective: the symmetric-window plumbing check of spa_comm_window_selftest."""
+        _check(load().spa_comm_window_selftest(self.h, nbytes), "spa_comm_window_selftest")
+
     def close(self):
         if self.h:
             load().spa_comm_destroy(self.h)
@@ -343,6 +351,21 @@ class Plan:
         self.ipc_open(ws, hs)
         dist.barrier(group=group)
 
+    # -- NCCL plans on an NCCL symmetric window (peer-memory exchange; spa_plan_window_register)
+    def window_setup(self, nbytes: Optional[int] = None, group=None) -> int:
+        """Collective: allocate this rank's workspace (nbytes, default workspace_bytes; e.g. qkv_workspace_bytes for
+        the fused-projection calls) with NCCL's allocator, register it as a symmetric window and barrier; returns the
+        device address to pass as ws (freed by close(), after the plan is destroyed)."""
+        import torch.distributed as dist
+        n = (max(nbytes if nbytes is not None else self.workspace_bytes, 1) + 4095) // 4096 * 4096
+        ptr = ctypes.c_void_p()
+        _check(load().spa_mem_alloc(n, ctypes.byref(ptr)), "spa_mem_alloc")
+        self._window_ws = ptr.value
+        _check(load().spa_plan_window_register(self.h, ctypes.c_void_p(ptr.value)), "spa_plan_window_register")
+        if dist.is_available() and dist.is_initialized():
+            dist.barrier(group=group)
+        return ptr.value
+
     # -- QKV projection (SURVEY f3)
     def qkv_weight_bytes(self, C: int) -> int:
         n = ctypes.c_size_t()
@@ -406,6 +429,9 @@ class Plan:
         if self.h:
             load().spa_plan_destroy(self.h)
             self.h = None
+        if getattr(self, "_window_ws", None):
+            load().spa_mem_free(ctypes.c_void_p(self._window_ws))
+            self._window_ws = None
 
 
 # ------------------------------------------------------------------ calls (same names as the C ABI)

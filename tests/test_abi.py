@@ -124,7 +124,10 @@ def test_stage_split_and_workspace():
         p = spa.Plan(comm, 1, 118_800, 24, 128, stages=st)
         assert p.stage_split == exp
         shard = 118_800 // 8 * 24 * 128 * 2
-        assert shard * 8 <= p.workspace_bytes < shard * 8 + 8 * 256
+        # 8 exchange shards + the direct transport's landing shard + the epoch-flag block (P2P / NCCL-window plans;
+        # DESIGN.md §4)
+        flags = 4 * 8 * (1 + 2 * exp[0] * exp[1])
+        assert shard * 9 + flags <= p.workspace_bytes < shard * 9 + flags + 10 * 256
 
 
 def _labels(B, S, H, D, P, n_src=None):
