@@ -101,7 +101,14 @@ struct Cfg {
 #endif
 #endif
     static constexpr bool NG4 = ((SPA_NG4_MASK >> (D == 64 ? 0 : (D == 96 ? 1 : 2))) & 1) != 0;
-    static constexpr int BN = NG4 ? 96 : 128;
+    // DP: "decoupled P" -- three chains of 96-key tiles whose bf16 P goes to two separate TMEM P buffers instead of over
+    // the scores, so a tile's S buffer is free as soon as pass 1 has read it (both halves stay in registers) and S(j+3)
+    // is issued then, not after PV(j): the MMA chain no longer waits for the softmax's exponentials.
+#ifndef SPA_DP_MASK
+#define SPA_DP_MASK 0   // bit 0: D = 64, bit 1: D = 96, bit 2: D = 128
+#endif
+    static constexpr bool DP = !NG4 && ((SPA_DP_MASK >> (D == 64 ? 0 : (D == 96 ? 1 : 2))) & 1) != 0;
+    static constexpr int BN = (NG4 || DP) ? 96 : 128;
     static constexpr int NG = NG4 ? 4 : 3;
     static constexpr int HALF = BN / 2;                  // keys per P release (64 or 48)
     static constexpr int NUM_SOFTMAX_WARPS = 4 * NG;
@@ -145,7 +152,8 @@ struct Cfg {
     static constexpr int XCH_BYTES = BM * 4;   // static smem: running max (the epilogue's (m, l) reuse ring slot 0)
     static constexpr int SMEM_BYTES = 1024 /*align slack*/ + TILE_BYTES + NS * HALF_BYTES + BAR_BYTES;
     static constexpr uint32_t TMEM_COLS = 512;
-    static constexpr uint32_t O_COL = BN * NG;           // O accumulator columns [O_COL, O_COL + D)
+    static constexpr uint32_t P_COL = BN * NG;           // DP: P buffers u = 0, 1 at [P_COL + u*HALF, +HALF)
+    static constexpr uint32_t O_COL = BN * NG + (DP ? BN : 0);   // O accumulator columns [O_COL, O_COL + D)
     static_assert(O_COL + D <= TMEM_COLS, "TMEM budget");
     static constexpr int OCHUNKS = D / 16;               // epilogue: 16-column chunks, chunk c by group c % NG
     // exp2 split: key pairs with (key & 15) >= POLY_FROM use the FMA-pipe polynomial, the rest MUFU.EX2
@@ -170,7 +178,8 @@ struct SmemBars {
     uint64_t kv_empty[16];
     uint64_t s_full[NG_MAX];       // [buffer]: S(j) complete
     uint64_t p_full[NG_MAX][2];    // [buffer][key half]: P(j) half written (leader's: 4 warps of the group, both CTAs)
-    uint64_t pv_done[NG_MAX];      // [buffer]: PV(j) complete (O may be rescaled)
+    uint64_t pv_done[NG_MAX];      // [buffer]: PV(j) complete (O may be rescaled); DP: [j % 4]
+    uint64_t s_free[NG_MAX];       // DP: [buffer]: S(j) read by the 8 softmax warps of the pair (S(j+NG) may overwrite it)
     uint64_t o_final;          // all PVs completed (epilogue)
     uint32_t tmem_base;
 };
@@ -241,7 +250,9 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1)
             ptx::mbar_init(&bars->p_full[t][0], 8);   // one arrival per softmax warp of that group, both CTAs
             ptx::mbar_init(&bars->p_full[t][1], 8);
             ptx::mbar_init(&bars->pv_done[t], 1);
+            ptx::mbar_init(&bars->s_free[t], 8);
         }
+        if (C::DP) ptx::mbar_init(&bars->pv_done[3], 1);   // DP: PV(j) completes on pv_done[j % 4]
         ptx::mbar_init(&bars->o_final, 1);
         ptx::fence_mbar_init();
     }
@@ -301,11 +312,12 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1)
             __syncwarp();
             ++cnt;
         };
-        // same order as the MMA issuer consumes: K0 .. K_{NG-1}, then V_j, K_{j+NG}
+        // same order as the MMA issuer consumes: K0 .. K_{NG-1}, then V_j, K_{j+NG} (DP: K_{j+NG}, V_j)
         for (int j = 0; j < NG && j < n_kv; ++j) load(false, j);
         for (int j = 0; j < n_kv; ++j) {
+            if (C::DP && j + NG < n_kv) load(false, j + NG);
             load(true, j);
-            if (j + NG < n_kv) load(false, j + NG);
+            if (!C::DP && j + NG < n_kv) load(false, j + NG);
         }
     } else if (warp == MMA_WARP) {
         // ------------------------------------------------------------ MMA issuer
@@ -363,13 +375,21 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1)
             for (int j = 0; j < n_kv; ++j) {
                 const int t = j % NG;
                 const uint32_t tS = tmem + t * BN;
+                if (C::DP && j + NG < n_kv) {   // S buffer t is free once the 8 softmax warps of tile j read it
+                    ptx::mbar_wait(&bars->s_free[t], (j / NG) & 1);
+                    ptx::tc_fence_after();
+                    issue_qk(j + NG);
+                }
+                // P(j): over the first HALF/2 columns of each half of S buffer t, or (DP) in P buffer j % 2
+                const uint32_t tPj = C::DP ? tmem + C::P_COL + (j & 1) * HALF : tS;
                 const int slotV = acquire();
                 if (leader) TRACE(j, 10);
                 const uint64_t dVs = dV + ((uint64_t)(slotV * C::HALF_BYTES) >> 4);
 #pragma unroll
                 for (int o = 0; o < 2; ++o) {
                     const int hf = HALF_ORDER[o];   // the key half the softmax releases o-th
-                    ptx::mbar_wait(&bars->p_full[t][hf], (j / NG) & 1);   // both CTAs' softmax warps
+                    if (C::DP) ptx::mbar_wait(&bars->p_full[j & 1][hf], (j >> 1) & 1);
+                    else ptx::mbar_wait(&bars->p_full[t][hf], (j / NG) & 1);   // both CTAs' softmax warps
                     ptx::tc_fence_after();
                     if (leader) {
                         TRACE(j, o);
@@ -378,18 +398,19 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1)
 #pragma unroll
                         for (int kk = 0; kk < HALF / 16; ++kk) {
                             const int key16 = hf * (HALF / 16) + kk;
-                            ptx::mma_ts2(tO, tS + hf * HALF + kk * 8, dVs + ((uint64_t)(key16 * 16 * rowb) >> 4),
+                            ptx::mma_ts2(tO, tPj + hf * (C::DP ? HALF / 2 : HALF) + kk * 8,
+                                         dVs + ((uint64_t)(key16 * 16 * rowb) >> 4),
                                          IDESC_PV, (j > 0 || o > 0 || kk > 0) ? 1u : 0u);
                         }
                         if (o == 1) {
                             ptx::mma_commit2_mc(&bars->kv_empty[slotV], PAIR_MASK);
-                            ptx::mma_commit2_mc(&bars->pv_done[t], PAIR_MASK);
+                            ptx::mma_commit2_mc(&bars->pv_done[C::DP ? (j & 3) : t], PAIR_MASK);
                             if (j == n_kv - 1) ptx::mma_commit2_mc(&bars->o_final, PAIR_MASK);
                         }
                     }
                     __syncwarp();
                 }
-                if (j + NG < n_kv) issue_qk(j + NG);
+                if (!C::DP && j + NG < n_kv) issue_qk(j + NG);
             }
         }
     } else if (warp >= C::SM_BASE && warp < C::SM_BASE + NUM_SOFTMAX_WARPS) {
@@ -421,16 +442,28 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1)
             TRACE2(j, crank * 4 + wq, 0);
             // pass 1: row max over the BN keys, two rounds of HALF columns; with 152 registers (NG = 3) the half
             // pass 2 processes first is read second and its scores stay in registers (kv) for pass 2
+            // (DP: both halves are read in one round and stay in registers; the S buffer is released right after)
             constexpr bool KEEP = NG == 3;
+            constexpr bool DP = C::DP;
             float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
-            uint32_t kv[HALF];
+            uint32_t kv[HALF], ka[HALF];   // ka: DP only (the half HALF_ORDER[1])
+            if (DP) {
+                ptx::tmem_ld_cols<HALF>(tS + HALF * HALF_ORDER[1], ka);
+                ptx::tmem_ld_cols<HALF>(tS + HALF * HALF_ORDER[0], kv);
+                ptx::tmem_wait_ld();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(&bars->s_free[g], 0));   // the leader's
+            }
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int h = HALF_ORDER[1 - r];
                 uint32_t tv[HALF];
-                uint32_t (&sv)[HALF] = (r && KEEP) ? kv : tv;
-                ptx::tmem_ld_cols<HALF>(tS + HALF * h, sv);
-                ptx::tmem_wait_ld();
+                uint32_t (&sv)[HALF] = DP ? (r ? kv : ka) : ((r && KEEP) ? kv : tv);
+                if (!DP) {
+                    ptx::tmem_ld_cols<HALF>(tS + HALF * h, sv);
+                    ptx::tmem_wait_ld();
+                }
                 if (masked) {
 #pragma unroll
                     for (int i = 0; i < HALF; ++i)
@@ -472,16 +505,19 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1)
                 // committed before S(j-1), which the previous group saw complete before handing over the max,
                 // and PV(j-1+NG) cannot complete before PV(j), which needs this group's P(j).
                 const int jp = j - 1;
-                ptx::mbar_wait(&bars->pv_done[jp % NG], (jp / NG) & 1);
+                // (DP: PV(j) completes on pv_done[j % 4]; PV(j-5) completed before S(j), so the parity is unambiguous)
+                if (DP) ptx::mbar_wait(&bars->pv_done[jp & 3], (jp >> 2) & 1);
+                else ptx::mbar_wait(&bars->pv_done[jp % NG], (jp / NG) & 1);
                 ptx::tc_fence_after();
-#pragma unroll
-                for (int c = 0; c < D / 32; ++c) {
-                    uint32_t r[32];
-                    ptx::tmem_ld32(tO + 32 * c, r);
+                constexpr int RC = DP ? 16 : 32;   // columns per round (DP holds 2 x HALF scores in registers)
+#pragma unroll 1
+                for (int c = 0; c < D / RC; ++c) {
+                    uint32_t r[RC];
+                    ptx::tmem_ld_cols<RC>(tO + RC * c, r);
                     ptx::tmem_wait_ld();
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * factor);
-                    ptx::tmem_st32(tO + 32 * c, r);
+                    for (int i = 0; i < RC; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * factor);
+                    ptx::tmem_st_cols<RC>(tO + RC * c, r);
                 }
             }
             // pass 2, per HALF-key half: P = exp2(s*sl2 - m) in f32x2 pairs (MUFU or FMA-pipe polynomial by
@@ -489,12 +525,18 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1)
             // the MMA issuer.
             const uint64_t NEGM = ptx::f2pack(-m, -m);
             uint64_t L0 = ptx::f2pack(0.f, 0.f), L1 = L0;
+            if (DP && j >= 2) {   // P buffer j % 2 is free once PV(j-2) completed (PV(j-6) did before S(j))
+                ptx::mbar_wait(&bars->pv_done[(j - 2) & 3], ((j - 2) >> 2) & 1);
+                ptx::tc_fence_after();
+            }
+            const uint32_t tP = DP ? tmem + lane_base + C::P_COL + (j & 1) * HALF : tS;
 #pragma unroll
             for (int o = 0; o < 2; ++o) {
                 const int h = HALF_ORDER[o];
                 uint32_t tv[HALF];
-                uint32_t (&sv)[HALF] = (o || !KEEP) ? tv : kv;   // KEEP: the first half is still in registers
-                if (o || !KEEP) {
+                // KEEP: the first half is still in registers; DP: both are
+                uint32_t (&sv)[HALF] = DP ? (o ? ka : kv) : ((o || !KEEP) ? tv : kv);
+                if ((o || !KEEP) && !DP) {
                     ptx::tmem_ld_cols<HALF>(tS + HALF * h, sv);
                     ptx::tmem_wait_ld();
                     if (masked) {
@@ -522,11 +564,11 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1)
                     else L0 = ptx::fadd2(L0, ptx::f2pack(p0, p1));
                     pk[i] = ptx::pack_bf16x2(p0, p1);
                 }
-                ptx::tmem_st_cols<HALF / 2>(tS + HALF * h, pk);
+                ptx::tmem_st_cols<HALF / 2>(tP + (DP ? HALF / 2 : HALF) * h, pk);
                 ptx::tmem_wait_st();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(&bars->p_full[g][h], 0));   // the leader's
+                if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(&bars->p_full[DP ? (j & 1) : g][h], 0));   // the leader's
                 if (tr && o == 0) TRACE(j, 8);
                 TRACE2(j, crank * 4 + wq, 1 + o);
             }
