@@ -294,3 +294,16 @@ def test_usp_messages_match(P, U):
     sub = [spa.Plan(spa.Comm.host(U, u), B, U * (S // P), H, D) for u in range(U)]
     for d in (0, 1):
         _match({u: sub[u].describe_messages(0, d, u) for u in range(U)}, U)
+
+
+def test_window_register_needs_an_nccl_plan():
+    """spa_plan_window_register (NCCL symmetric windows) refuses host plans and NULL arguments before
+    touching any device; the direct option is accepted at set-up on NCCL-like plans and checked at the call."""
+    lib = spa.load()
+    p = spa.Plan(spa.Comm.host(4, 1), 1, 64, 8, 64, stages=2)
+    assert lib.spa_plan_window_register(p.h, ctypes.c_void_p(4096)) == 1   # SPA_ERR_INVALID: not an NCCL plan
+    assert b"NCCL" in lib.spa_last_error()
+    assert lib.spa_plan_window_register(p.h, None) == 1
+    assert lib.spa_mem_free(None) == 0
+    p.set_option(spa.SPA_OPT_DIRECT, 1)
+    p.close()
