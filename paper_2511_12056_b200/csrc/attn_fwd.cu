@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1)
             ptx::mbar_init(&bars->p_full[t][0], 8);   // one arrival per softmax warp of that group, both CTAs
             ptx::mbar_init(&bars->p_full[t][1], 8);
             ptx::mbar_init(&bars->pv_done[t], 1);
-            ptx::mbar_init(&bars->s_free[t], 8);
+            if (C::DP) ptx::mbar_init(&bars->s_free[t], 8);   // one arrival per softmax warp of the pair
         }
         if (C::DP) ptx::mbar_init(&bars->pv_done[3], 1);   // DP: PV(j) completes on pv_done[j % 4]
         ptx::mbar_init(&bars->o_final, 1);
@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(Cfg<D>::NUM_THREADS, 1)
                 else ptx::mbar_wait(&bars->pv_done[jp % NG], (jp / NG) & 1);
                 ptx::tc_fence_after();
                 constexpr int RC = DP ? 16 : 32;   // columns per round (DP holds 2 x HALF scores in registers)
-#pragma unroll 1
+#pragma unroll
                 for (int c = 0; c < D / RC; ++c) {
                     uint32_t r[RC];
                     ptx::tmem_ld_cols<RC>(tO + RC * c, r);
