@@ -39,7 +39,7 @@ __device__ __forceinline__ void ex2_poly2(uint64_t X, float &y0, float &y1) {
 // with no TMEM traffic in the loop (scores stay in registers, P folded into a checksum); 5: the kernel with the
 // second half's TMEM load issued before the first half is processed; 6: the kernel without the row-sum FADD2s (as if
 // the tensor core summed P); 7: 6 with f16x2 MUFU exponentials for the MUFU pairs (x packed to f16x2, P stays f16:
-// the exp cost of an f16-P design)
+// the exp cost of an f16-P design); 8: single load round (all 128 scores in registers, no reload in pass 2)
 template <int MODE, int POLY_FROM, int NT>
 __global__ void __launch_bounds__(NT, 1) k(unsigned long long *out, float *sink) {
     __shared__ uint32_t tbase;
@@ -70,12 +70,18 @@ __global__ void __launch_bounds__(NT, 1) k(unsigned long long *out, float *sink)
     for (int it = 0; it < ITER; ++it) {
         float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
         uint32_t kv[HALF];
+        uint32_t ka[HALF];
+        if (MODE == 8) {
+            ptx::tmem_ld_cols<HALF>(tS, ka);
+            ptx::tmem_ld_cols<HALF>(tS + HALF, kv);
+            ptx::tmem_wait_ld();
+        }
         if (MODE != 1 && MODE != 3) {
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 uint32_t tv[HALF];
-                uint32_t (&sv)[HALF] = MODE == 4 ? regs[1 - r] : (r ? kv : tv);
-                if (MODE != 4) {
+                uint32_t (&sv)[HALF] = MODE == 4 ? regs[1 - r] : (MODE == 8 ? (r ? kv : ka) : (r ? kv : tv));
+                if (MODE != 4 && MODE != 8) {
                     ptx::tmem_ld_cols<HALF>(tS + HALF * (1 - r), sv);
                     ptx::tmem_wait_ld();
                 }
@@ -100,8 +106,8 @@ __global__ void __launch_bounds__(NT, 1) k(unsigned long long *out, float *sink)
         for (int o = 0; o < 2; ++o) {
             const int h = 1 - o;   // HALF_ORDER = {1, 0}
             uint32_t tv[HALF];
-            const bool load = (o || MODE == 1 || MODE == 3) && MODE != 4;
-            uint32_t (&sv)[HALF] = MODE == 4 ? regs[h] : ((MODE == 5 && o) ? nx : (load ? tv : kv));
+            const bool load = (o || MODE == 1 || MODE == 3) && MODE != 4 && MODE != 8;
+            uint32_t (&sv)[HALF] = MODE == 4 ? regs[h] : (MODE == 8 ? (o ? ka : kv) : ((MODE == 5 && o) ? nx : (load ? tv : kv)));
             if (load) {
                 if (MODE != 5) ptx::tmem_ld_cols<HALF>(tS + HALF * h, sv);
                 ptx::tmem_wait_ld();
@@ -190,6 +196,11 @@ void run(const char *name, int W) {
 }
 
 int main() {
+    for (int W = 1; W <= 3; ++W) {
+        run<8, 12>("one_load_round", W);
+        run<8, 10>("one_load_round", W);
+        run<0, 12>("kernel", W);
+    }
     for (int W = 3; W <= 3; ++W) {
         run<6, 12>("no_rowsum", W);
         run<6, 10>("no_rowsum", W);
