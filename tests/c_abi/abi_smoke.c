@@ -2,6 +2,7 @@
  * validation errors and the stage split / workspace / message descriptions of a PipeSP plan, and the
  * padding helper.  Built and run by tests/test_abi.py::test_plain_c_client (CPU only, no GPU calls). */
 #include <stdio.h>
+#include <stdint.h>
 #include <string.h>
 
 #include "spa.h"
@@ -55,6 +56,9 @@ int main(void) {
     /* host-buffer SP workspace = the plan's + device copies of this rank's Q, K, V, O */
     size_t hb = 0;
     CHECK(spa_plan_host_sp_workspace_bytes(plan, &hb) == SPA_OK && hb >= ws + (size_t)4 * 14850 * 24 * 128 * 2, "hostbuf ws");
+    /* NCCL symmetric windows are for NCCL plans only (refused here before any device call); free(NULL) is a no-op */
+    CHECK(spa_plan_window_register(plan, (void *)(uintptr_t)4096) == SPA_ERR_INVALID, "window: not an NCCL plan");
+    CHECK(spa_mem_free(NULL) == SPA_OK, "mem_free(NULL)");
     CHECK(spa_plan_destroy(plan) == SPA_OK, "destroy plan");
     /* a ring plan: step 0 of rank 3 sends K, V to rank 4 and receives from rank 2 */
     spa_shape rs;
