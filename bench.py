@@ -89,6 +89,7 @@ class ClockSampler:
     def __init__(self, gpu_index: int, period_s: float = 0.02):
         self.gpu, self.period = gpu_index, period_s
         self.sm, self.reasons, self.max_mhz = [], set(), None
+        self.power_w, self.power_limit_w = [], None
         self._stop = threading.Event()
         self._t = None
 
@@ -100,8 +101,16 @@ class ClockSampler:
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
             get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
                 pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            try:
+                self.power_limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(h) / 1000.0
+            except Exception:  # pragma: no cover
+                pass
             while not self._stop.is_set():
                 self.sm.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                try:
+                    self.power_w.append(pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0)
+                except Exception:  # pragma: no cover
+                    pass
                 bits = get_reasons(h)
                 for bit, name in self.REASONS.items():
                     if bits & bit:
@@ -123,7 +132,9 @@ class ClockSampler:
 
     def summary(self):
         return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 20 ms, timed region"}
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 20 ms, timed region",
+                "power_w": statistics.median(self.power_w) if self.power_w else None,
+                "power_limit_w": self.power_limit_w}
 
 
 # ------------------------------------------------------------------ CPU oracle timing
