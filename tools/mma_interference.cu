@@ -34,7 +34,7 @@ __device__ __forceinline__ void ex2_poly2(uint64_t X, float &y0, float &y1) {
     ptx::f2unpack(ptx::fmul2(P, ptx::f2pack(s0, s1)), y0, y1);
 }
 
-// AUX: 0 = warp 3 idle, 1 = warp 3 issues MMAs in bursts of 8, 2 = warp 3 spins on an mbarrier
+// AUX: 0 = warp 3 idle, 1 = warp 3 issues SS MMAs in bursts of 8, 2 = warp 3 spins on an mbarrier, 3 = TS MMAs
 template <int AUX>
 __global__ void __launch_bounds__(512, 1) k(unsigned long long *out, float *sink, int mma_batches) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -153,6 +153,22 @@ __global__ void __launch_bounds__(512, 1) k(unsigned long long *out, float *sink
             ptx::mbar_wait(&bar, phase);
             phase ^= 1;
         }
+    } else if (warp == 3 && AUX == 3) {   // TS form (A from TMEM columns [448, 512), like the kernel's PV reading P)
+        const uint32_t sa = ptx::smem_u32(smem);
+        const bool leader = ptx::elect_one();
+        int phase = 0;
+        for (int b = 0; b < mma_batches && done < 12; ++b) {
+            if (leader) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    ptx::mma_ts(tm + 384, tm + 448 + i * 8, ptx::smem_desc(sa + (i & 3) * 2048, 16, 1024, 2),
+                                ptx::idesc_bf16(128, 64, 0, 1), i ? 1u : 0u);
+                ptx::mma_commit(&bar);
+            }
+            __syncwarp();
+            ptx::mbar_wait(&bar, phase);
+            phase ^= 1;
+        }
     } else if (warp == 3 && AUX == 2) {
         while (done < 12) ptx::mbar_try_wait(&never, 0);
     }
@@ -186,6 +202,7 @@ int main() {
     run<0>("idle");
     run<1>("mma_bursts_of_8");
     run<2>("spin_try_wait");
+    run<3>("mma_ts_bursts_of_8");
     run<0>("idle");
     return 0;
 }
