@@ -58,6 +58,8 @@ def parse():
                     help="layer from hidden states: fused QKV projection (f3) + PipeSP; FLOPs include the projection")
     ap.add_argument("--north-star", type=int, default=-1,
                     help="720p N_st sweep block: 1 on, 0 off, -1 (default) on when N == 8")
+    ap.add_argument("--no-one-rank", action="store_true",
+                    help="N=1: skip the north-star block measured as ONE rank's share of the 8-GPU schedule")
     return ap.parse_args()
 
 
@@ -231,6 +233,61 @@ def _a2a_send_bytes(plan, rank):
         for d in (0, 1):
             n += sum(m.bytes for m in plan.describe_messages(k, d, rank) if not m.is_recv and m.peer != rank)
     return n
+
+
+def north_star_one_rank(spa, synthgen, torch, peak, flush, P=8, stages=(1, 3, 24), reps=3):
+    """One rank's share of the 8-GPU PipeSP layer at 720p (BASELINE configs[3]), measured on one GPU: per stage split,
+    the layer time with no exchange, with the exchange moved by the copy kernel (NCCL-like SM transport) and with the
+    direct peer stores, exposed %, and the fraction of the overlapped roofline max(FLOPs/peak, bytes sent/900 GB/s)."""
+    w = synthgen.WORKLOADS["hy720p129f"]
+    B, S, H, D = w.B, w.S, w.H, w.D
+    S_l = S // P
+    shards = [[synthgen.gen_qkv_shard(0, t, (B, S, H, D), q * S_l, (q + 1) * S_l, device="cuda") for q in range(P)]
+              for t in range(3)]
+    outs = [torch.empty_like(x) for x in shards[0]]
+    fl_rank = attn_flops(B, S, H, D) / P
+    rows = []
+    for st in stages:
+        plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=st)
+        ws = plan.workspace()
+        sent = _a2a_send_bytes(plan, 0)
+        troof = max(fl_rank / (peak * 1e12), sent / (NVLINK_GBS * 1e9)) * 1e3
+        spa.spa_pipesp_attention_local(plan, *shards, outs, ws)   # every buffer holds real data first
+        torch.cuda.synchronize()
+        res = {}
+        for mode in ("skip", "kernel", "direct"):
+            plan.set_option(spa.SPA_OPT_RANK_ONLY, 1)
+            plan.set_option(spa.SPA_OPT_DIRECT, int(mode == "direct"))
+            plan.set_option(spa.SPA_OPT_SKIP_COMM, int(mode == "skip"))
+            for _ in range(2):
+                spa.spa_pipesp_attention_local(plan, *shards, outs, ws)
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(reps):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                spa.spa_pipesp_attention_local(plan, *shards, outs, ws)
+                b.record()
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            res[mode] = statistics.median(ts)
+        for mode in ("kernel", "direct"):
+            rows.append({"stages": st, "stage_split": list(plan.stage_split), "transport": mode,
+                         "ms_per_layer": res[mode], "ms_no_exchange": res["skip"],
+                         "exposed_a2a_pct": max(0.0, 100.0 * (res[mode] - res["skip"]) / res[mode]),
+                         "tflops_per_gpu": fl_rank / (res[mode] * 1e-3) / 1e12,
+                         "frac_overlapped_roofline": troof / res[mode], "t_roofline_ms": troof,
+                         "bytes_sent_per_rank": sent})
+        plan.close()
+        del ws
+    del shards, outs
+    best = max(rows, key=lambda r: r["frac_overlapped_roofline"])
+    return {"workload": "hy720p129f", "P": P, "rank": 0, "best": best, "rows": rows,
+            "what": "one rank's share of the 8-GPU layer measured on ONE GPU (loopback plan, SPA_OPT_RANK_ONLY): "
+                    "its attention stages, pack/unpack and the bytes it sends / receives as local copies or direct "
+                    "stores; NVLink time of those bytes at 900 GB/s enters the roofline",
+            "target": ">= 0.60 of the overlapped roofline, <= 10 % exposed all-to-all (BASELINE.json)"}
 
 
 def run_ours(args):
@@ -492,6 +549,14 @@ def run_ours(args):
         north = {"workload": "hy720p129f", "P": P, "best": best, "sweep": sweep,
                  "target": ">= 0.60 of the overlapped roofline, <= 10 % exposed all-to-all (BASELINE.json)"}
 
+    # ---------------------------------------------------------------- north star, one rank's share (N = 1)
+    # BASELINE configs[3] (720p, P = 8) cannot run on one GPU; its per-rank schedule can: a loopback plan over 8 virtual
+    # ranks with SPA_OPT_RANK_ONLY runs only rank 0's launches and the messages rank 0 sends or receives through the
+    # real scheduler (tools/rank_schedule.py).  Labelled as such; not the bench value.
+    one_rank = None
+    if P == 1 and not args.no_one_rank and not args.qkv:
+        one_rank = north_star_one_rank(spa, synthgen, torch, peak, flush)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = time_oracle(S, D, args.cpu_seconds)
@@ -513,6 +578,7 @@ def run_ours(args):
             "exposed_a2a_pct": exposed, "ms_skip_comm": t_nocomm, "a2a": a2a, "overlapped_roofline": overlapped,
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches,
             "roofline": roofline, "cpu_baseline": cpu, "north_star": north, "qkv_projection": qkv_info,
+            "north_star_one_rank": one_rank,
         }
         print(json.dumps(line), flush=True)
     comm.close()
