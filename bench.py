@@ -290,6 +290,52 @@ def north_star_one_rank(spa, synthgen, torch, peak, flush, P=8, stages=(1, 3, 24
             "target": ">= 0.60 of the overlapped roofline, <= 10 % exposed all-to-all (BASELINE.json)"}
 
 
+def aco_one_rank(spa, synthgen, torch, flush, P=8, n_src=6, reps=3):
+    """BASELINE configs[4] (Aco: 720p attention over 6 denoising + 2 decoding GPUs) measured as single
+    ranks' shares on one GPU: a source rank and a co-processor rank of the 6 + 2 plan against one rank of PipeSP on the
+    6 denoising GPUs alone; speed-up vs Eq. 3's ideal N / N_d = 8 / 6 for t_L = 0.  Staged
+    exchange by the copy kernel, one stage."""
+    w = synthgen.WORKLOADS["hy720p129f"]
+    B, S, H, D = w.B, w.S, w.H, w.D
+    S_l = S // n_src
+    shards = [[synthgen.gen_qkv_shard(0, t, (B, S, H, D), q * S_l, (q + 1) * S_l, device="cuda") for q in range(n_src)]
+              for t in range(3)]
+    outs = [torch.empty_like(x) for x in shards[0]]
+
+    def one(plan, call, rank):
+        ws = plan.workspace()
+        call(plan, *shards, outs, ws)   # every buffer holds real data first
+        torch.cuda.synchronize()
+        plan.set_option(spa.SPA_OPT_RANK_ONLY, rank + 1)
+        for _ in range(2):
+            call(plan, *shards, outs, ws)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            call(plan, *shards, outs, ws)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        plan.set_option(spa.SPA_OPT_RANK_ONLY, 0)
+        del ws
+        return statistics.median(ts)
+
+    aco = spa.Plan(spa.Comm.loopback(P), B, S, H, D, n_src=n_src)
+    t_src = one(aco, spa.spa_aco_attention_local, 0)
+    t_cop = one(aco, spa.spa_aco_attention_local, P - 1)
+    aco.close()
+    pip = spa.Plan(spa.Comm.loopback(n_src), B, S, H, D)
+    t_pip = one(pip, spa.spa_pipesp_attention_local, 0)
+    pip.close()
+    del shards, outs
+    return {"workload": "hy720p129f", "P": P, "n_src": n_src, "ms_source_rank": t_src, "ms_coprocessor_rank": t_cop,
+            "ms_pipesp_on_n_src_gpus": t_pip, "speedup": t_pip / max(t_src, t_cop), "eq3_ideal": P / n_src,
+            "what": "single ranks' shares measured on ONE GPU (loopback plans, SPA_OPT_RANK_ONLY), copy-kernel exchange"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -553,9 +599,10 @@ def run_ours(args):
     # BASELINE configs[3] (720p, P = 8) cannot run on one GPU; its per-rank schedule can: a loopback plan over 8 virtual
     # ranks with SPA_OPT_RANK_ONLY runs only rank 0's launches and the messages rank 0 sends or receives through the
     # real scheduler (tools/rank_schedule.py).  Labelled as such; not the bench value.
-    one_rank = None
+    one_rank = aco = None
     if P == 1 and not args.no_one_rank and not args.qkv:
         one_rank = north_star_one_rank(spa, synthgen, torch, peak, flush)
+        aco = aco_one_rank(spa, synthgen, torch, flush)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -578,7 +625,7 @@ def run_ours(args):
             "exposed_a2a_pct": exposed, "ms_skip_comm": t_nocomm, "a2a": a2a, "overlapped_roofline": overlapped,
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches,
             "roofline": roofline, "cpu_baseline": cpu, "north_star": north, "qkv_projection": qkv_info,
-            "north_star_one_rank": one_rank,
+            "north_star_one_rank": one_rank, "aco_one_rank": aco,
         }
         print(json.dumps(line), flush=True)
     comm.close()
