@@ -336,6 +336,30 @@ def aco_one_rank(spa, synthgen, torch, flush, P=8, n_src=6, reps=3):
             "what": "single ranks' shares measured on ONE GPU (loopback plans, SPA_OPT_RANK_ONLY), copy-kernel exchange"}
 
 
+def single_gpu_config(spa, synthgen, torch, peak, flush, workload="osp480p93f", reps=5):
+    """Another BASELINE configuration's whole layer on this one GPU (the attention kernel over all heads), CUDA events,
+    L2 flushed before each of `reps` launches: ms, TF/s and the fraction of the measured peak."""
+    w = synthgen.WORKLOADS[workload]
+    q, k, v = (synthgen.gen_qkv_shard(0, t, (w.B, w.S, w.H, w.D), 0, w.S, device="cuda") for t in range(3))
+    o = torch.empty_like(q)
+    for _ in range(3):
+        spa.attention(q, k, v, o)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        spa.attention(q, k, v, o)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = statistics.median(ts)
+    tf = attn_flops(w.B, w.S, w.H, w.D) / (ms * 1e-3) / 1e12
+    return {"workload": workload, "B": w.B, "S": w.S, "H": w.H, "D": w.D, "ms_per_layer": ms, "tflops": tf,
+            "frac_of_peak": tf / peak}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -599,10 +623,12 @@ def run_ours(args):
     # BASELINE configs[3] (720p, P = 8) cannot run on one GPU; its per-rank schedule can: a loopback plan over 8 virtual
     # ranks with SPA_OPT_RANK_ONLY runs only rank 0's launches and the messages rank 0 sends or receives through the
     # real scheduler (tools/rank_schedule.py).  Labelled as such; not the bench value.
-    one_rank = aco = None
+    one_rank = aco = other = None
     if P == 1 and not args.no_one_rank and not args.qkv:
         one_rank = north_star_one_rank(spa, synthgen, torch, peak, flush)
         aco = aco_one_rank(spa, synthgen, torch, flush)
+    if P == 1 and not args.qkv and name != "osp480p93f":   # configs[1] on this GPU, next to the headline
+        other = single_gpu_config(spa, synthgen, torch, peak, flush)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -625,7 +651,7 @@ def run_ours(args):
             "exposed_a2a_pct": exposed, "ms_skip_comm": t_nocomm, "a2a": a2a, "overlapped_roofline": overlapped,
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches,
             "roofline": roofline, "cpu_baseline": cpu, "north_star": north, "qkv_projection": qkv_info,
-            "north_star_one_rank": one_rank, "aco_one_rank": aco,
+            "north_star_one_rank": one_rank, "aco_one_rank": aco, "osp_single_gpu": other,
         }
         print(json.dumps(line), flush=True)
     comm.close()
