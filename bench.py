@@ -623,12 +623,19 @@ def run_ours(args):
     # BASELINE configs[3] (720p, P = 8) cannot run on one GPU; its per-rank schedule can: a loopback plan over 8 virtual
     # ranks with SPA_OPT_RANK_ONLY runs only rank 0's launches and the messages rank 0 sends or receives through the
     # real scheduler (tools/rank_schedule.py).  Labelled as such; not the bench value.
+    def extra(fn, *a):   # informational blocks: a failure there is reported in the line, never fatal to the bench
+        try:
+            return fn(*a)
+        except Exception as e:  # pragma: no cover
+            torch.cuda.synchronize()
+            return {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+
     one_rank = aco = other = None
     if P == 1 and not args.no_one_rank and not args.qkv:
-        one_rank = north_star_one_rank(spa, synthgen, torch, peak, flush)
-        aco = aco_one_rank(spa, synthgen, torch, flush)
+        one_rank = extra(north_star_one_rank, spa, synthgen, torch, peak, flush)
+        aco = extra(aco_one_rank, spa, synthgen, torch, flush)
     if P == 1 and not args.qkv and name != "osp480p93f":   # configs[1] on this GPU, next to the headline
-        other = single_gpu_config(spa, synthgen, torch, peak, flush)
+        other = extra(single_gpu_config, spa, synthgen, torch, peak, flush)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
