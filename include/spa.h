@@ -165,8 +165,8 @@ spa_status spa_plan_ipc_open(spa_plan *plan, void *ws, const uint8_t *handles);
  *      (ncclMemAlloc: the memory NCCL can map into its peers)
  *   2. every rank: spa_plan_window_register(plan, ws) -- COLLECTIVE over the plan's communicator
  *      (ncclCommWindowRegister, NCCL_WIN_COLL_SYMMETRIC); resolves every rank's address of its window with NCCL's
- *      device API (ncclGetLsaPointer) and zeroes this rank's flags.  SPA_ERR_COMM if a rank is outside the caller's
- *      NVLink domain; SPA_ERR_UNSUPPORTED for ring / USP plans (they keep NCCL send / recv); 1-rank plans: no-op.
+ *      device API (ncclGetLsaPointer) and zeroes this rank's flags.  SPA_ERR_UNSUPPORTED if the communicator's LSA
+ *      team (ncclDevCommCreate: the ranks NCCL maps into each other, one NVLink domain) is not all ranks; SPA_ERR_UNSUPPORTED for ring / USP plans (they keep NCCL send / recv); 1-rank plans: no-op.
  *   3. a host barrier over all ranks before the first call
  * Afterwards every call passes this ws; spa_plan_destroy deregisters the window; spa_mem_free(ws) after that.
  * SPA_OPT_DIRECT on an NCCL plan requires the window (SPA_ERR_INVALID at the call otherwise).  Validation status:

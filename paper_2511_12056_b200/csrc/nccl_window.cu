@@ -45,6 +45,18 @@ cudaError_t nccl_window_bases(ncclWindow_t w, int n, uint8_t **bases, cudaStream
     return e;
 }
 
+// The communicator's LSA team (the ranks NCCL maps into each other's address space -- one NVLink domain): size and
+// this rank's index in it, from a device communicator with no resource requirements (collective).
+ncclResult_t nccl_lsa_team(ncclComm_t comm, int *lsa_size, int *lsa_rank) {
+    ncclDevCommRequirements_t reqs = {};
+    ncclDevComm_t dc = {};
+    ncclResult_t r = ncclDevCommCreate(comm, &reqs, &dc);
+    if (r != ncclSuccess) return r;
+    *lsa_size = dc.lsaSize;
+    *lsa_rank = dc.lsaRank;
+    return ncclDevCommDestroy(comm, &dc);
+}
+
 cudaError_t nccl_window_fill_pattern(uint32_t *lsa_self, long long n_words, uint32_t seed, cudaStream_t st) {
     lsa_pattern_kernel<<<148, 256, 0, st>>>(lsa_self, n_words, seed);
     return cudaGetLastError();

@@ -161,6 +161,7 @@ struct spa_plan {
 namespace spa {
 cudaError_t nccl_window_bases(ncclWindow_t w, int n, uint8_t **bases, cudaStream_t st);   // nccl_window.cu
 cudaError_t nccl_window_fill_pattern(uint32_t *lsa_self, long long n_words, uint32_t seed, cudaStream_t st);
+ncclResult_t nccl_lsa_team(ncclComm_t comm, int *lsa_size, int *lsa_rank);
 }  // namespace spa
 namespace {
 
@@ -1514,6 +1515,12 @@ spa_status spa_plan_window_register(spa_plan *plan, void *ws) {
     if (reinterpret_cast<uintptr_t>(ws) % NCCL_WIN_REQUIRED_ALIGNMENT)
         return fail(SPA_ERR_INVALID, "NCCL window: ws must be 4096-byte aligned (spa_mem_alloc)");
     SPA_CHECK_CUDA(cudaSetDevice(plan->comm->device));
+    // every rank must be in this rank's NVLink domain, with LSA index = world rank (the peer addresses below)
+    int lsa_size = 0, lsa_rank = -1;
+    SPA_CHECK_NCCL(nccl_lsa_team(plan->comm->nccl, &lsa_size, &lsa_rank));
+    if (lsa_size != plan->comm->nranks || lsa_rank != plan->comm->rank)
+        return fail(SPA_ERR_UNSUPPORTED, "NCCL window: the ranks do not form one NVLink domain (LSA team " +
+                                             std::to_string(lsa_size) + " of " + std::to_string(plan->comm->nranks) + ")");
     const size_t bytes = (size_t)align_up(plan->ws_rank_bytes, NCCL_WIN_REQUIRED_ALIGNMENT);
     ncclWindow_t w = nullptr;
     SPA_CHECK_NCCL(ncclCommWindowRegister(plan->comm->nccl, ws, bytes, &w, NCCL_WIN_COLL_SYMMETRIC));
@@ -1549,6 +1556,10 @@ spa_status spa_comm_window_selftest(spa_comm *comm, size_t bytes) {
     if (!comm || comm->kind != KIND_NCCL || !comm->nccl) return fail(SPA_ERR_INVALID, "not an NCCL comm");
     if (bytes < 4096 || bytes % 4096) return fail(SPA_ERR_INVALID, "bytes: a positive multiple of 4096");
     SPA_CHECK_CUDA(cudaSetDevice(comm->device));
+    int lsa_size = 0, lsa_rank = -1;
+    SPA_CHECK_NCCL(nccl_lsa_team(comm->nccl, &lsa_size, &lsa_rank));
+    if (lsa_size != comm->nranks || lsa_rank != comm->rank)
+        return fail(SPA_ERR_UNSUPPORTED, "window self-test: the LSA team is not the whole communicator");
     void *buf = nullptr;
     SPA_CHECK_NCCL(ncclMemAlloc(&buf, bytes));
     ncclWindow_t w = nullptr;
