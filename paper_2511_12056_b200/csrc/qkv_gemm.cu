@@ -7,6 +7,8 @@
 // Wp holds one head group's rows of the fused weight in [tensor t][dest rank q][r < g*D] order (packed once per
 // plan by spa_plan_pack_qkv_weight), so column n = (t*P + q)*g*D + r lands at
 //   dst[t] + q*q_stride + m*row_stride + r       (bf16, RNE from the fp32 accumulator + fp32 bias)
+// or, with the direct transport, at peer[q] + off[t] + row'(m)*row_stride + r: destination rank q's receive region over
+// peer memory (NVLink), so the projection, the pack and the input all-to-all are one kernel.
 // which is send_t[kh][q][b][t][jj][d] for the stage's head group -- or, for a 1-rank plan, the
 // plain [B, S, H, D] Q/K/V tensors.
 //
@@ -199,8 +201,15 @@ __global__ void __launch_bounds__(GTHREADS, 1)
                     const int rem = n - t * args.cols_per_t;
                     const int q = rem / args.cols_per_q;
                     const int rr = rem - q * args.cols_per_q;
-                    __nv_bfloat16 *base = t == 0 ? args.dst[0] : (t == 1 ? args.dst[1] : args.dst[2]);
-                    uint4 *dst = reinterpret_cast<uint4 *>(base + q * args.q_stride + m * args.row_stride + rr);
+                    __nv_bfloat16 *base;
+                    long long row = m;
+                    if (args.peer[0]) {   // direct: destination rank q's receive region (peer memory)
+                        base = args.peer[q] + (t == 0 ? args.off[0] : (t == 1 ? args.off[1] : args.off[2]));
+                        row = (long long)(m / args.rows_per_b) * args.batch_rows + m % args.rows_per_b;
+                    } else {
+                        base = (t == 0 ? args.dst[0] : (t == 1 ? args.dst[1] : args.dst[2])) + q * args.q_stride;
+                    }
+                    uint4 *dst = reinterpret_cast<uint4 *>(base + row * args.row_stride + rr);
                     dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
                     dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
                     dst[2] = make_uint4(w[8], w[9], w[10], w[11]);
@@ -280,6 +289,10 @@ cudaError_t launch_qkv_gemm(const QkvProblem &p, cudaStream_t st) {
     for (int t = 0; t < 3; ++t) a.dst[t] = reinterpret_cast<__nv_bfloat16 *>(p.dst[t]);
     a.q_stride = p.q_stride; a.row_stride = p.row_stride;
     a.cols_per_t = p.cols_per_t; a.cols_per_q = p.cols_per_q;
+    for (int q = 0; q < kMaxDst; ++q) a.peer[q] = reinterpret_cast<__nv_bfloat16 *>(p.peer[q]);
+    for (int t = 0; t < 3; ++t) a.off[t] = p.off[t];
+    a.rows_per_b = p.rows_per_b > 0 ? p.rows_per_b : 1;
+    a.batch_rows = p.batch_rows;
     const int usable = sms - (p.reserve_sms > 0 ? p.reserve_sms : 0);
     const int clusters = std::max(1, std::min(a.tiles, usable / 2));
     cudaLaunchConfig_t cfg{};

@@ -424,6 +424,33 @@ spa_status launch_qkv(spa_plan *p, const void *x, const uint8_t *wp, int C, int 
     return SPA_OK;
 }
 
+// Head group kh's projections of source rank r stored straight into every owner's receive regions (direct transport
+// with the fused projections, one query chunk): peers[q] = owner q's workspace (local virtual rank or peer memory).
+spa_status launch_qkv_direct(spa_plan *p, const Split &s, const void *x, const uint8_t *wp, int C, int r, int kh,
+                             uint8_t *const peers[], cudaStream_t st) {
+    QkvProblem g{};
+    g.x = x;
+    g.w = wp + (long long)kh * qkv_cols(p) * C * 2;
+    g.bias = reinterpret_cast<const float *>(wp + qkv_bias_off(p, C)) + (long long)kh * qkv_cols(p);
+    g.M = p->sh.B * p->len[r];
+    g.N = (int)qkv_cols(p);
+    g.K = C;
+    g.row_stride = (long long)s.g * p->sh.D;
+    g.cols_per_q = s.g * p->sh.D;
+    g.cols_per_t = p->P * g.cols_per_q;
+    g.reserve_sms = p->comm_sms;
+    for (int q = 0; q < p->P; ++q) g.peer[q] = peers[q];
+    g.off[0] = p->off_recvQ / 2 + idx_qo(p, s, kh, 0, 0, r);   // [kh][c=0][b][S][g][D]: this source's rows
+    g.off[1] = p->off_recvK / 2 + idx_kv(p, s, kh, 0, r);      // [kh][b][S][g][D]
+    g.off[2] = p->off_recvV / 2 + idx_kv(p, s, kh, 0, r);
+    g.rows_per_b = p->len[r];
+    g.batch_rows = p->sh.S;
+    cudaError_t e = launch_qkv_gemm(g, st);
+    if (e != cudaSuccess) return fail(SPA_ERR_CUDA, std::string("qkv gemm (direct): ") + cudaGetErrorString(e));
+    ++p->gemm_launches;
+    return SPA_OK;
+}
+
 // The exchange runs on peer memory: CUDA-IPC (P2P) plans, and NCCL plans with a registered symmetric window.
 bool peer_mem(const spa_plan *p) { return p->comm->kind == KIND_P2P || p->win != nullptr; }
 
@@ -795,7 +822,16 @@ spa_status execute_direct(Exec &x) {
     pr.begin("pack", x.sc);
     std::vector<CopyJob> jobs;
     const long long offs[3] = {p->off_recvQ, p->off_recvK, p->off_recvV};
-    for (int r = 0; r < p->Psrc; ++r) {
+    if (x.qkv) {   // the fused projections store every owner's pieces themselves (projection + pack + exchange)
+        std::vector<uint8_t *> peers(p->P);
+        for (int q = 0; q < p->P; ++q) peers[q] = resolve(x, q, BUF_WS, 0);
+        for (int kh = 0; kh < s.G_h; ++kh)
+            for (int r = 0; r < p->Psrc; ++r) {
+                if (p->rank_only >= 0 && r != p->rank_only) continue;
+                SPA_TRY(launch_qkv_direct(p, s, x.xin[r], x.wp, x.C, r, kh, peers.data(), x.sc));
+            }
+    }
+    for (int r = 0; r < p->Psrc && !x.qkv; ++r) {
         if (p->rank_only >= 0 && r != p->rank_only) continue;
         const void *xs[3] = {x.ptr.q[r], x.ptr.k[r], x.ptr.v[r]};
         const long long n = p->len[r];
@@ -906,7 +942,19 @@ spa_status execute_direct_p2p(Exec &x) {
     pr.begin("pack", x.sc);
     std::vector<CopyJob> jobs;
     const long long offs[3] = {p->off_recvQ, p->off_recvK, p->off_recvV};
-    if (is_source(p, me)) {
+    // fused projections (one query chunk): head group kh's GEMM stores into every owner, then flags stage kh
+    std::vector<cudaEvent_t> ev_grp;
+    if (x.qkv && is_source(p, me)) {
+        std::vector<uint8_t *> peers(p->P);
+        for (int q = 0; q < p->P; ++q) peers[q] = resolve(x, q, BUF_WS, 0);
+        for (int kh = 0; kh < s.G_h; ++kh) {
+            SPA_TRY(launch_qkv_direct(p, s, x.xin[0], x.wp, x.C, me, kh, peers.data(), x.sc));
+            if (!p->skip_comm) SPA_TRY(p2p_signal(p, x.sc, FLAG_IN, kh));
+            ev_grp.push_back(p->sync_ev[4 + kh]);
+            SPA_CHECK_CUDA(cudaEventRecord(ev_grp.back(), x.sc));
+        }
+    }
+    if (is_source(p, me) && !x.qkv) {
         const void *xs[3] = {x.ptr.q[0], x.ptr.k[0], x.ptr.v[0]};
         const long long n = p->len[me];
         for (int t = 0; t < 3; ++t)
@@ -944,7 +992,7 @@ spa_status execute_direct_p2p(Exec &x) {
     }
     if (!jobs.empty()) SPA_CHECK_CUDA(launch_copy_jobs(jobs.data(), (int)jobs.size(), x.sc, &p->copy_launches));
     pr.end("pack", x.sc);
-    if (!p->skip_comm) {
+    if (!p->skip_comm && !x.qkv) {
         SPA_TRY(p2p_signal(p, x.sc, FLAG_IN, 0));   // all of this rank's runs are in place (every stage)
         SPA_TRY(p2p_wait(p, x.sc, FLAG_IN, 0));
     }
@@ -959,6 +1007,10 @@ spa_status execute_direct_p2p(Exec &x) {
         cudaStream_t st;
         SPA_TRY(stage_stream(p, x.sc, k, &st));
         if (st != x.sc && st != p->sc_alt) SPA_CHECK_CUDA(cudaStreamWaitEvent(st, ev_pack, 0));
+        if (x.qkv) {   // this head group's pieces: the own GEMM's stores and every peer's flag for stage k (= kh)
+            if (kh < (int)ev_grp.size()) SPA_CHECK_CUDA(cudaStreamWaitEvent(st, ev_grp[kh], 0));
+            if (!p->skip_comm) SPA_TRY(p2p_wait(p, st, FLAG_IN, k));
+        }
         pr.begin(an, st);
         const int nreal = real_heads(p, s, me, kh);
         if (nreal > 0) {
@@ -1019,7 +1071,9 @@ spa_status execute(Exec &x) {
     const Split &s = *x.s;
     const int N = s.n();
     SPA_TRY(ensure_events(p, 4 + 3 * (size_t)N + 3 * (size_t)s.G_h, p->profile ? 8 + 6 * (size_t)N : 0));
-    if (p->direct && p->P > 1 && x.has_attn && x.has_pack && x.has_out && !x.qkv && !x.host)
+    // direct transport: the pack (or, with one query chunk, the fused projections) and the attention epilogue store to
+    // the owners / sources themselves
+    if (p->direct && p->P > 1 && x.has_attn && x.has_pack && x.has_out && !x.host && (!x.qkv || s.C == 1))
         return peer_mem(p) ? execute_direct_p2p(x) : execute_direct(x);
     Prof pr{p};
     if (p->P == 1) {

@@ -70,6 +70,13 @@ struct QkvProblem {
     long long q_stride, row_stride;
     int cols_per_t, cols_per_q;
     int reserve_sms;
+    // Direct transport (peer[0] != NULL; SURVEY f1 for the projections): column block q of tensor t goes straight into
+    // destination rank q's receive region, peer[q] + off[t] + row'*row_stride + r (elements), with the batch remap
+    // row' = (m / rows_per_b) * batch_rows + m % rows_per_b (this source's rows of batch entry b inside the owner's
+    // [b][S] rows); dst / q_stride are then unused.
+    void *peer[kMaxDst] = {};
+    long long off[3] = {};
+    int rows_per_b = 1, batch_rows = 1;
 };
 struct QkvArgs {
     int M, N, K, tiles_n, tiles;
@@ -77,6 +84,9 @@ struct QkvArgs {
     __nv_bfloat16 *dst[3];
     long long q_stride, row_stride;
     int cols_per_t, cols_per_q;
+    __nv_bfloat16 *peer[kMaxDst];
+    long long off[3];
+    int rows_per_b, batch_rows;
 };
 cudaError_t launch_qkv_gemm(const QkvProblem &p, cudaStream_t st);
 

@@ -172,3 +172,29 @@ def test_fullsize_720p_p8():
         ref = oracle.attention_rows(q[0, rows, h].double().cpu().numpy(), k[0, :, h].double().cpu().numpy(),
                                     v[0, :, h].double().cpu().numpy())
         U.assert_close(out[0, rows, h], ref)
+
+
+@pytest.mark.parametrize("P,stages,B,S,H,D,C", [
+    (2, 1, 1, 512, 4, 64, 256), (2, 2, 2, 512, 4, 128, 512), (4, 2, 2, 1000, 8, 96, 384),
+    (8, 3, 1, 2048, 24, 64, 1536), (3, 2, 1, 1001, 6, 64, 384), (4, 4, 1, 1024, 8, 128, 1024),
+])
+def test_fused_direct_equals_staged(P, stages, B, S, H, D, C):
+    """Direct transport with the fused projections (SURVEY f1 + f3): each head group's GEMM stores its columns
+    straight into every owner's receive regions (projection + pack + input all-to-all in one kernel) -- the same bits
+    as the staged fused call, for uneven shards and B > 1 too."""
+    X, W, b = _inputs(B, S, C, H, D, seed=17 + P + stages)
+    staged = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=stages)
+    wp = staged.pack_qkv_weight(W, b)
+    ref = _fused(P, X, wp, C, H, D, stages, staged)
+    direct = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=stages)
+    direct.set_option(spa.SPA_OPT_DIRECT, 1)
+    direct.set_option(spa.SPA_OPT_PROFILE, 1)
+    out = _fused(P, X, wp, C, H, D, stages, direct)
+    assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
+    prof = direct.last_profile()
+    G_h, n_chunks, _ = direct.stage_split
+    assert prof.gemm_launches == G_h * P
+    if n_chunks == 1:   # the GEMMs moved every byte: no pack / exchange / unpack copies
+        assert prof.copy_launches == 0
+    else:               # query chunks: the staged transport is used
+        assert prof.copy_launches > 0
