@@ -428,6 +428,7 @@ spa_status launch_qkv(spa_plan *p, const void *x, const uint8_t *wp, int C, int 
 // with the fused projections, one query chunk): peers[q] = owner q's workspace (local virtual rank or peer memory).
 spa_status launch_qkv_direct(spa_plan *p, const Split &s, const void *x, const uint8_t *wp, int C, int r, int kh,
                              uint8_t *const peers[], cudaStream_t st) {
+    if (p->P > kMaxDst) return fail(SPA_ERR_UNSUPPORTED, "direct projections: at most 16 owners");
     QkvProblem g{};
     g.x = x;
     g.w = wp + (long long)kh * qkv_cols(p) * C * 2;
