@@ -283,11 +283,10 @@ spa_status spa_pipesp_attention_hostbuf_local(spa_plan *plan, const void *const 
  * tcgen05 GEMM computes this rank's X [B, S_r, C] times the head group's weight rows for EVERY destination rank and
  * stores the result (fp32 accumulate + fp32 bias, bf16 RNE) straight into the stage's all-to-all send layout (the
  * pack step is fused away); head group kh's input all-to-all then overlaps head group kh+1's GEMM, and the rest is
- * spa_pipesp_attention.  Plans: Ulysses / PipeSP (n_src = 0, no head padding, no ring).  SPA_OPT_DIRECT with a
- * stage split without query chunks (N_st dividing h): each head group's GEMM stores its columns straight into every
- * owner's receive regions (loopback: the virtual ranks' workspaces; P2P / NCCL-window plans: the peers' over NVLink) --
- * projection, pack and input all-to-all in one kernel -- and flags the stage to the owners; same bits.  With query
- * chunks the staged transport is used.  Result = spa_pipesp_attention on bf16(X W^T + b), bit for bit.
+ * spa_pipesp_attention.  Plans: Ulysses / PipeSP (n_src = 0, no head padding, no ring).  With SPA_OPT_DIRECT each
+ * head group's GEMM stores its columns straight into every owner's receive regions (loopback: the virtual ranks'
+ * workspaces; P2P / NCCL-window plans: the peers' over NVLink; Q rows into their query chunk's stage, up to 32 chunks)
+ * -- projection, pack and input all-to-all in one kernel -- and flags the group's stages to the owners; same bits.  Result = spa_pipesp_attention on bf16(X W^T + b), bit for bit.
  *
  *   w      bf16 [3*H*D, C], the fused nn.Linear weight: output feature o = t*H*D + k*D + d (t = 0 Q, 1 K, 2 V;
  *          head k; dim d).  bias: fp32 [3*H*D] or NULL.  C: hidden dim, a positive multiple of 8.

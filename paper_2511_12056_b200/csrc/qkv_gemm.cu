@@ -204,8 +204,16 @@ __global__ void __launch_bounds__(GTHREADS, 1)
                     __nv_bfloat16 *base;
                     long long row = m;
                     if (args.peer[0]) {   // direct: destination rank q's receive region (peer memory)
-                        base = args.peer[q] + (t == 0 ? args.off[0] : (t == 1 ? args.off[1] : args.off[2]));
-                        row = (long long)(m / args.rows_per_b) * args.batch_rows + m % args.rows_per_b;
+                        const int bb = m / args.rows_per_b, tt = m - bb * args.rows_per_b;
+                        if (t == 0 && args.q_chunks > 1) {   // Q row tt -> its query chunk's stage region
+                            const int c = (int)(((long long)(tt + 1) * args.q_chunks - 1) / args.rows_per_b);
+                            const int lo = (int)((long long)c * args.rows_per_b / args.q_chunks);
+                            base = args.peer[q] + args.q_chunk_off[c];
+                            row = (long long)bb * args.q_chunk_rows[c] + (tt - lo);
+                        } else {
+                            base = args.peer[q] + (t == 0 ? args.off[0] : (t == 1 ? args.off[1] : args.off[2]));
+                            row = (long long)bb * args.batch_rows + tt;
+                        }
                     } else {
                         base = (t == 0 ? args.dst[0] : (t == 1 ? args.dst[1] : args.dst[2])) + q * args.q_stride;
                     }
@@ -293,6 +301,9 @@ cudaError_t launch_qkv_gemm(const QkvProblem &p, cudaStream_t st) {
     for (int t = 0; t < 3; ++t) a.off[t] = p.off[t];
     a.rows_per_b = p.rows_per_b > 0 ? p.rows_per_b : 1;
     a.batch_rows = p.batch_rows;
+    if (p.q_chunks < 1 || p.q_chunks > kMaxQChunks) return cudaErrorInvalidValue;
+    a.q_chunks = p.q_chunks;
+    for (int c = 0; c < kMaxQChunks; ++c) { a.q_chunk_off[c] = p.q_chunk_off[c]; a.q_chunk_rows[c] = p.q_chunk_rows[c]; }
     const int usable = sms - (p.reserve_sms > 0 ? p.reserve_sms : 0);
     const int clusters = std::max(1, std::min(a.tiles, usable / 2));
     cudaLaunchConfig_t cfg{};

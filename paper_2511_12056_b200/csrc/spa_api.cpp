@@ -446,6 +446,12 @@ spa_status launch_qkv_direct(spa_plan *p, const Split &s, const void *x, const u
     g.off[2] = p->off_recvV / 2 + idx_kv(p, s, kh, 0, r);
     g.rows_per_b = p->len[r];
     g.batch_rows = p->sh.S;
+    if (s.C > kMaxQChunks) return fail(SPA_ERR_UNSUPPORTED, "direct projections: at most 32 query chunks");
+    g.q_chunks = s.C;
+    for (int c = 0; c < s.C; ++c) {   // chunk c of this source: stage (kh, c), after the earlier sources' pieces
+        g.q_chunk_off[c] = p->off_recvQ / 2 + idx_qo(p, s, kh, c, 0, r);
+        g.q_chunk_rows[c] = (int)Lstage(p, s, c);
+    }
     cudaError_t e = launch_qkv_gemm(g, st);
     if (e != cudaSuccess) return fail(SPA_ERR_CUDA, std::string("qkv gemm (direct): ") + cudaGetErrorString(e));
     ++p->gemm_launches;
@@ -943,14 +949,15 @@ spa_status execute_direct_p2p(Exec &x) {
     pr.begin("pack", x.sc);
     std::vector<CopyJob> jobs;
     const long long offs[3] = {p->off_recvQ, p->off_recvK, p->off_recvV};
-    // fused projections (one query chunk): head group kh's GEMM stores into every owner, then flags stage kh
+    // fused projections: head group kh's GEMM stores into every owner, then flags the group's stages
     std::vector<cudaEvent_t> ev_grp;
     if (x.qkv && is_source(p, me)) {
         std::vector<uint8_t *> peers(p->P);
         for (int q = 0; q < p->P; ++q) peers[q] = resolve(x, q, BUF_WS, 0);
         for (int kh = 0; kh < s.G_h; ++kh) {
             SPA_TRY(launch_qkv_direct(p, s, x.xin[0], x.wp, x.C, me, kh, peers.data(), x.sc));
-            if (!p->skip_comm) SPA_TRY(p2p_signal(p, x.sc, FLAG_IN, kh));
+            for (int c = 0; c < s.C && !p->skip_comm; ++c)   // every query chunk (stage) of head group kh
+                SPA_TRY(p2p_signal(p, x.sc, FLAG_IN, kh * s.C + c));
             ev_grp.push_back(p->sync_ev[4 + kh]);
             SPA_CHECK_CUDA(cudaEventRecord(ev_grp.back(), x.sc));
         }
@@ -1008,7 +1015,7 @@ spa_status execute_direct_p2p(Exec &x) {
         cudaStream_t st;
         SPA_TRY(stage_stream(p, x.sc, k, &st));
         if (st != x.sc && st != p->sc_alt) SPA_CHECK_CUDA(cudaStreamWaitEvent(st, ev_pack, 0));
-        if (x.qkv) {   // this head group's pieces: the own GEMM's stores and every peer's flag for stage k (= kh)
+        if (x.qkv) {   // this stage's pieces: the own GEMM's stores (head group kh) and every peer's flag for stage k
             if (kh < (int)ev_grp.size()) SPA_CHECK_CUDA(cudaStreamWaitEvent(st, ev_grp[kh], 0));
             if (!p->skip_comm) SPA_TRY(p2p_wait(p, st, FLAG_IN, k));
         }
@@ -1074,7 +1081,7 @@ spa_status execute(Exec &x) {
     SPA_TRY(ensure_events(p, 4 + 3 * (size_t)N + 3 * (size_t)s.G_h, p->profile ? 8 + 6 * (size_t)N : 0));
     // direct transport: the pack (or, with one query chunk, the fused projections) and the attention epilogue store to
     // the owners / sources themselves
-    if (p->direct && p->P > 1 && x.has_attn && x.has_pack && x.has_out && !x.host && (!x.qkv || s.C == 1))
+    if (p->direct && p->P > 1 && x.has_attn && x.has_pack && x.has_out && !x.host && (!x.qkv || s.C <= kMaxQChunks))
         return peer_mem(p) ? execute_direct_p2p(x) : execute_direct(x);
     Prof pr{p};
     if (p->P == 1) {

@@ -8,6 +8,7 @@
 namespace spa {
 
 constexpr int kMaxDst = 16;   // ranks one attention launch can scatter its output rows to
+constexpr int kMaxQChunks = 32;   // query chunks per head group the direct projection GEMM can address
 
 // Attention problem for one launch (a head group of one stage, or a whole single-GPU layer).
 // Element (b, s, j, d) of q is at q + b*q_batch_stride + s*q_tok_stride + j*D + d (elements).
@@ -77,6 +78,12 @@ struct QkvProblem {
     void *peer[kMaxDst] = {};
     long long off[3] = {};
     int rows_per_b = 1, batch_rows = 1;
+    // Query chunks (C > 1): Q row t of this source lies in chunk c = ((t+1)*C - 1) / rows_per_b, i.e. rows
+    // [c*rows_per_b/C, (c+1)*rows_per_b/C), and goes to q_chunk_off[c] + (b*q_chunk_rows[c] + t - first row of c)
+    // (elements, relative to peer[q]); off[0] and batch_rows are then not used for Q.
+    int q_chunks = 1;
+    long long q_chunk_off[kMaxQChunks] = {};
+    int q_chunk_rows[kMaxQChunks] = {};
 };
 struct QkvArgs {
     int M, N, K, tiles_n, tiles;
@@ -87,6 +94,9 @@ struct QkvArgs {
     __nv_bfloat16 *peer[kMaxDst];
     long long off[3];
     int rows_per_b, batch_rows;
+    int q_chunks;
+    long long q_chunk_off[kMaxQChunks];
+    int q_chunk_rows[kMaxQChunks];
 };
 cudaError_t launch_qkv_gemm(const QkvProblem &p, cudaStream_t st);
 

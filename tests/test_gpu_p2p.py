@@ -58,6 +58,7 @@ _port_cache = [0]
     (2, dict(B=1, S=2048, H=4, D=128, stages=2, qkv=True)),       # f3 over the P2P transport
     (2, dict(B=1, S=2048, H=4, D=128, stages=2, qkv=True, direct=True)),   # projection GEMM stores into the peers
     (4, dict(B=2, S=3001, H=8, D=64, stages=2, qkv=True, direct=True)),
+    (4, dict(B=1, S=4099, H=8, D=128, stages=8, qkv=True, direct=True)),   # + query chunks (C = 4)
     (8, dict(B=1, S=8192, H=24, D=128, stages=3)),
     (2, dict(B=1, S=2048, H=3, D=128, ring=True)),                # Ring-Attention over P2P (R21, any H)
     (4, dict(B=2, S=4096, H=5, D=64, ring=True)),

@@ -96,8 +96,6 @@ def main():
             torch.cuda.synchronize()
             res = {}
             for mode in args.modes.split(","):
-                if args.qkv and mode == "direct" and plan.stage_split[1] > 1:
-                    continue   # the fused projections store to the owners only without query chunks
                 plan.set_option(spa.SPA_OPT_RANK_ONLY, r + 1)
                 plan.set_option(spa.SPA_OPT_LOOPBACK_CE, int(mode == "ce"))
                 plan.set_option(spa.SPA_OPT_DIRECT, int(mode == "direct"))
