@@ -155,6 +155,15 @@ def test_fullsize_720p_p8():
     plan = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=3)
     wp = plan.pack_qkv_weight(W, b)
     out = _fused(P, X, wp, C, H, D, 3, plan)
+    # the direct transport at full size: the projection GEMMs store into the owners (N_st = 3 and, with query chunks,
+    # N_st = 24) -- the same bits
+    for st in (3, 24):
+        dp = spa.Plan(spa.Comm.loopback(P), B, S, H, D, stages=st)
+        dp.set_option(spa.SPA_OPT_DIRECT, 1)
+        od = _fused(P, X, dp.pack_qkv_weight(W, b), C, H, D, st, dp)
+        assert torch.equal(od.view(torch.int16), out.view(torch.int16)), st
+        dp.close()
+        del od
     del wp
     p1 = spa.Plan(spa.Comm.loopback(1), B, S, H, D)
     wp1 = p1.pack_qkv_weight(W, b)
